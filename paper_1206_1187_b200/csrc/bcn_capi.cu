@@ -1,0 +1,734 @@
+// bcn_capi.cu — the extern "C" boundary (include/bcnrand_b200.h).
+//
+// Host responsibilities: validate exactly like the reference (before any
+// device work), translate the reference's plan semantics (make_plan,
+// physical_index, base_offset wrap) into affine exponent segments and
+// interleaved regions, and launch the sm_100a kernels of bcn_kernels.cu.
+// Host output buffers are filled by generating chunks on the device and
+// copying them back (two streams, generation overlapped with D2H).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/bcnrand_b200.h"
+#include "bcn_kernels.cuh"
+
+using namespace bcn_b200;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+bcn_status fail(bcn_status st, const std::string& msg) {
+    g_last_error = msg;
+    return st;
+}
+
+bcn_status cuda_fail(cudaError_t e, const char* where) {
+    return fail(BCN_ERR_CUDA, std::string(where) + ": " + cudaGetErrorName(e) + " (" +
+                                  cudaGetErrorString(e) + ")");
+}
+
+#define BCN_CUDA(call)                                   \
+    do {                                                 \
+        cudaError_t e_ = (call);                         \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+    } while (0)
+
+// ----------------------------------------------------------- plan (host)
+// reference parallel.cpp:35-52 / :19-33
+struct Plan {
+    uint64_t n = 0;
+    uint64_t wpw = 0;
+    uint32_t workers = 1;
+    int layout = 0;
+    uint64_t elements_for(uint32_t w) const {
+        const uint64_t start = static_cast<uint64_t>(w) * wpw;
+        return std::min(wpw, n - start);
+    }
+    uint64_t short_count() const { return elements_for(workers - 1); }
+};
+
+bcn_status make_plan(uint64_t n, uint32_t workers, int layout, Plan* p) {
+    if (n == 0) return fail(BCN_ERR_INVALID_ARGUMENT, "make_plan: n must be at least 1");
+    if (workers == 0) return fail(BCN_ERR_INVALID_ARGUMENT, "make_plan: workers must be at least 1");
+    p->n = n;
+    p->wpw = (n + workers - 1) / workers;
+    p->workers = static_cast<uint32_t>((n + p->wpw - 1) / p->wpw);
+    p->layout = layout;
+    return BCN_OK;
+}
+
+bcn_status check_seed(uint64_t a) {
+    if (a < kMinSeed || a > kMaxSeed)
+        return fail(BCN_ERR_OUT_OF_RANGE, "seed_from_index: index outside [3^33+100, 2^53]");
+    return BCN_OK;
+}
+
+// ------------------------------------------------------- device context
+struct DevCtx {
+    bool init = false;
+    int sms = 148;
+    cudaStream_t stream = nullptr;    // internal stream for stream == NULL calls
+    cudaStream_t copy[2] = {nullptr, nullptr};
+    void* scratch[2] = {nullptr, nullptr};  // device chunks for host outputs
+    void* pinned[2] = {nullptr, nullptr};   // pinned staging for pageable outputs
+    size_t chunk_bytes = 0;
+    unsigned long long* digest = nullptr;
+    int* flag = nullptr;
+    std::map<int, int> occ;           // (fmt*8+engine) -> blocks per SM
+    std::mutex mu;                    // serialises host-buffer fills on this device
+};
+
+std::mutex g_ctx_mu;
+std::map<int, DevCtx*> g_ctx;
+
+bcn_status get_ctx(int device, DevCtx** out) {
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+        return fail(BCN_ERR_CUDA, "no CUDA device available (the B200 path has no CPU fallback)");
+    if (device < 0 || device >= count)
+        return fail(BCN_ERR_INVALID_ARGUMENT, "device ordinal out of range");
+    BCN_CUDA(cudaSetDevice(device));
+    std::lock_guard<std::mutex> lock(g_ctx_mu);
+    DevCtx*& c = g_ctx[device];
+    if (!c) c = new DevCtx();
+    if (!c->init) {
+        BCN_CUDA(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device));
+        BCN_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        BCN_CUDA(cudaStreamCreateWithFlags(&c->copy[0], cudaStreamNonBlocking));
+        BCN_CUDA(cudaStreamCreateWithFlags(&c->copy[1], cudaStreamNonBlocking));
+        BCN_CUDA(cudaMalloc(&c->digest, 3 * sizeof(unsigned long long)));
+        BCN_CUDA(cudaMalloc(&c->flag, sizeof(int)));
+        BCN_CUDA(upload_tables());
+        c->init = true;
+    }
+    *out = c;
+    return BCN_OK;
+}
+
+int resolve_engine(int engine, int fmt) {
+    if (engine != kEngAuto) return engine;
+    (void)fmt;
+    return kEngBarrett;  // measured best (profiles/)
+}
+
+int blocks_per_sm(DevCtx* c, int fmt, int engine, bool interleaved) {
+    const int key = (interleaved ? 64 : 0) + fmt * 8 + engine;
+    auto it = c->occ.find(key);
+    if (it != c->occ.end()) return it->second;
+    const int n = interleaved ? interleaved_blocks_per_sm(fmt, engine, kContigThreads)
+                              : contig_blocks_per_sm(fmt, engine, kContigThreads);
+    c->occ[key] = n;
+    return n;
+}
+
+int grid_for_rows(DevCtx* c, int fmt, int engine, bool interleaved, uint64_t rows) {
+    const uint64_t persistent = static_cast<uint64_t>(c->sms) * blocks_per_sm(c, fmt, engine, interleaved);
+    const uint64_t needed = (rows + (kContigThreads / 32) - 1) / (kContigThreads / 32);
+    return static_cast<int>(std::max<uint64_t>(1, std::min(persistent, needed)));
+}
+
+uint64_t mod_p(unsigned __int128 x) { return static_cast<uint64_t>(x % kPeriod); }
+
+// Exponent of 2 (mod P) for logical element j when every element from 0 is on
+// one affine segment whose first state is next(state_at(a, k0)).
+uint64_t exp_add(uint64_t e, uint64_t j) { return mod_p(static_cast<unsigned __int128>(e) + mod_p(static_cast<unsigned __int128>(j) * 53u)); }
+
+// Jump multiplier for a signed number of logical steps.
+Mult mult_for_steps(__int128 steps) {
+    __int128 s = steps % static_cast<__int128>(kPeriod);
+    if (s < 0) s += kPeriod;
+    return host_make_mult(host_jump(static_cast<uint64_t>(s)));
+}
+
+// ------------------------------------------------------------- launching
+struct FillJob {
+    const Plan* plan;
+    int fmt;
+    int engine;
+    uint64_t a;
+    uint64_t base_offset;
+    uint64_t a_exp;  // (a - 3^33 - 1) mod P
+    DevCtx* ctx;
+    cudaStream_t stream;
+};
+
+cudaError_t enqueue_slots(const FillJob& j, char* dptr, uint64_t slot0, uint64_t count) {
+    if (count == 0) return cudaSuccess;
+    SlotArgs s;
+    s.out = dptr;
+    s.slot0 = slot0;
+    s.count = count;
+    s.n = j.plan->n;
+    s.wpw = j.plan->wpw;
+    s.workers = j.plan->workers;
+    s.layout = j.plan->layout;
+    s.a_exp = j.a_exp;
+    s.base_offset = j.base_offset;
+    return launch_slots(j.fmt, s, j.stream);
+}
+
+// Physical slots [slot0, slot0+count) whose logical exponents are affine:
+// slot slot0 + x has exponent (e_first + 53 x) mod P.
+cudaError_t enqueue_affine(const FillJob& j, char* dptr, uint64_t slot0, uint64_t count,
+                           uint64_t e_first) {
+    const int isz = format_itemsize(j.fmt);
+    const uint64_t addr = reinterpret_cast<uint64_t>(dptr);
+    if (j.engine == kEngStaged) {
+        const uint64_t tile = static_cast<uint64_t>(kStagedThreads) * kStagedL;
+        const uint64_t head = std::min<uint64_t>(count, ((16 - addr % 16) % 16) / isz);
+        const uint64_t tiles = (count - head) / tile;
+        cudaError_t e = enqueue_slots(j, dptr, slot0, head);
+        if (e != cudaSuccess) return e;
+        if (tiles) {
+            StagedArgs s;
+            s.out = dptr + head * isz;
+            s.tiles = tiles;
+            s.e0 = exp_add(e_first, head);
+            const int grid = static_cast<int>(std::min<uint64_t>(tiles, static_cast<uint64_t>(j.ctx->sms) * 3));
+            s.jump_next = mult_for_steps(static_cast<__int128>(grid) * tile - kStagedL);
+            e = launch_staged(j.fmt, s, grid, j.stream);
+            if (e != cudaSuccess) return e;
+        }
+        const uint64_t done = head + tiles * tile;
+        return enqueue_slots(j, dptr + done * isz, slot0 + done, count - done);
+    }
+    const uint64_t row = 32ull * (32 / isz);
+    const uint64_t head = std::min<uint64_t>(count, ((32 - addr % 32) % 32) / isz);
+    const uint64_t rows = (count - head) / row;
+    cudaError_t e = enqueue_slots(j, dptr, slot0, head);
+    if (e != cudaSuccess) return e;
+    if (rows) {
+        ContigArgs c;
+        c.out = dptr + head * isz;
+        c.rows = rows;
+        c.e0 = exp_add(e_first, head);
+        c.jump_row = mult_for_steps(static_cast<__int128>(row));
+        const int grid = grid_for_rows(j.ctx, j.fmt, j.engine, false, rows);
+        e = launch_contig(j.fmt, j.engine, c, grid, kContigThreads, j.stream);
+        if (e != cudaSuccess) return e;
+    }
+    const uint64_t done = head + rows * row;
+    return enqueue_slots(j, dptr + done * isz, slot0 + done, count - done);
+}
+
+// Interleaved region slots: region-relative slots [q_begin, q_begin+count)
+// of a region of `width` workers starting at element i_base; dptr is slot
+// q_begin; slot0 is its global physical slot (for the slot kernel).
+cudaError_t enqueue_region(const FillJob& j, char* dptr, uint64_t slot0, uint64_t q_begin,
+                           uint64_t count, uint64_t width, uint64_t i_base, uint64_t e_elem0) {
+    const Plan& p = *j.plan;
+    if (width == 1) {
+        // Worker 0 only: logical j = i_base + q, affine.
+        return enqueue_affine(j, dptr, slot0, count, exp_add(e_elem0, i_base + q_begin));
+    }
+    const int isz = format_itemsize(j.fmt);
+    const int engine = j.engine == kEngStaged ? kEngBarrett : j.engine;
+    const uint64_t addr = reinterpret_cast<uint64_t>(dptr);
+    const uint64_t row = 32ull * (32 / isz);
+    const uint64_t head = std::min<uint64_t>(count, ((32 - addr % 32) % 32) / isz);
+    const uint64_t rows = (count - head) / row;
+    cudaError_t e = enqueue_slots(j, dptr, slot0, head);
+    if (e != cudaSuccess) return e;
+    if (rows) {
+        InterleavedArgs r;
+        r.out = dptr + head * isz;
+        r.rows = rows;
+        r.q0 = q_begin + head;
+        r.width = width;
+        r.i_base = i_base;
+        r.wpw = p.wpw;
+        r.e0 = e_elem0;
+        const uint64_t adv_a = row / width;
+        r.adv_b = row % width;
+        // Same physical row: w += b, i += a -> logical += b*wpw + a.
+        r.jump_same = mult_for_steps(static_cast<__int128>(r.adv_b) * p.wpw + adv_a);
+        // Crossing a physical row: w += b - width, i += a + 1.
+        r.jump_wrap = mult_for_steps((static_cast<__int128>(r.adv_b) - static_cast<__int128>(width)) *
+                                         static_cast<__int128>(p.wpw) +
+                                     adv_a + 1);
+        const int grid = grid_for_rows(j.ctx, j.fmt, engine, true, rows);
+        e = launch_interleaved(j.fmt, engine, r, grid, kContigThreads, j.stream);
+        if (e != cudaSuccess) return e;
+    }
+    const uint64_t done = head + rows * row;
+    return enqueue_slots(j, dptr + done * isz, slot0 + done, count - done);
+}
+
+// Writes physical slots [p0, p1) of the plan into dptr (dptr == slot p0).
+cudaError_t enqueue_range(const FillJob& j, char* dptr, uint64_t p0, uint64_t p1) {
+    const Plan& p = *j.plan;
+    const int isz = format_itemsize(j.fmt);
+    const uint64_t last_start = static_cast<uint64_t>(p.workers - 1) * p.wpw;
+    const bool wraps = j.base_offset > UINT64_MAX - last_start;
+    if (p.layout == 0) {
+        // Affine segments: workers whose k_w = B + start_w does not wrap, then
+        // those that do (reference u64 arithmetic, parallel.cpp:63-64).
+        uint64_t cut = p.n;  // first slot of the wrapped segment
+        if (wraps) {
+            const unsigned __int128 room = (static_cast<unsigned __int128>(1) << 64) - j.base_offset;
+            const uint64_t wstar = static_cast<uint64_t>((room + p.wpw - 1) / p.wpw);
+            cut = std::min<uint64_t>(p.n, wstar * p.wpw);
+        }
+        const uint64_t e_seg0 = host_fill_e0(j.a, j.base_offset);
+        if (p0 < cut) {
+            const uint64_t end = std::min(p1, cut);
+            cudaError_t e = enqueue_affine(j, dptr, p0, end - p0, exp_add(e_seg0, p0));
+            if (e != cudaSuccess) return e;
+        }
+        if (p1 > cut) {
+            const uint64_t begin = std::max(p0, cut);
+            const uint64_t e_seg1 = host_fill_e0(j.a, j.base_offset + cut);  // wrapped k
+            return enqueue_affine(j, dptr + (begin - p0) * isz, begin, p1 - begin,
+                                  exp_add(e_seg1, begin - cut));
+        }
+        return cudaSuccess;
+    }
+    if (wraps) return enqueue_slots(j, dptr, p0, p1 - p0);  // exact, slow, rare
+    const uint64_t e0 = host_fill_e0(j.a, j.base_offset);
+    const uint64_t sc = p.short_count();
+    const uint64_t main = sc * p.workers;
+    if (p0 < main) {
+        const uint64_t end = std::min(p1, main);
+        cudaError_t e = enqueue_region(j, dptr, p0, p0, end - p0, p.workers, 0, e0);
+        if (e != cudaSuccess) return e;
+    }
+    if (p1 > main) {
+        const uint64_t begin = std::max(p0, main);
+        return enqueue_region(j, dptr + (begin - p0) * isz, begin, begin - main, p1 - begin,
+                              p.workers - 1, sc, e0);
+    }
+    return cudaSuccess;
+}
+
+bcn_status validate_enums(int fmt, int layout, int method, int engine) {
+    if (fmt < 0 || fmt > 2) return fail(BCN_ERR_INVALID_ARGUMENT, "fill: unknown format");
+    if (layout < 0 || layout > 1) return fail(BCN_ERR_INVALID_ARGUMENT, "fill: unknown layout");
+    if (method < 0 || method > 3) return fail(BCN_ERR_INVALID_ARGUMENT, "fill: unknown method");
+    if (engine < 0 || engine > 4) return fail(BCN_ERR_INVALID_ARGUMENT, "fill: unknown engine");
+    return BCN_OK;
+}
+
+bcn_status ensure_scratch(DevCtx* c, size_t bytes, bool pinned) {
+    if (c->chunk_bytes < bytes) {
+        for (int i = 0; i < 2; ++i) {
+            if (c->scratch[i]) cudaFree(c->scratch[i]);
+            if (c->pinned[i]) cudaFreeHost(c->pinned[i]);
+            c->scratch[i] = c->pinned[i] = nullptr;
+        }
+        c->chunk_bytes = bytes;
+    }
+    for (int i = 0; i < 2; ++i) {
+        if (!c->scratch[i]) BCN_CUDA(cudaMalloc(&c->scratch[i], c->chunk_bytes));
+        if (pinned && !c->pinned[i]) BCN_CUDA(cudaMallocHost(&c->pinned[i], c->chunk_bytes));
+    }
+    return BCN_OK;
+}
+
+// Host output: generate chunks on the device, D2H on alternating streams.
+bcn_status fill_host(FillJob& j, char* out, bool out_pinned) {
+    DevCtx* c = j.ctx;
+    std::lock_guard<std::mutex> lock(c->mu);
+    const int isz = format_itemsize(j.fmt);
+    const uint64_t chunk_items = (64ull << 20) / isz;  // 64 MiB per chunk
+    bcn_status st = ensure_scratch(c, chunk_items * isz, !out_pinned);
+    if (st) return st;
+    const uint64_t n = j.plan->n;
+    const uint64_t nchunks = (n + chunk_items - 1) / chunk_items;
+    for (uint64_t k = 0; k < nchunks; ++k) {
+        const int b = static_cast<int>(k & 1);
+        const uint64_t p0 = k * chunk_items, p1 = std::min(n, p0 + chunk_items);
+        j.stream = c->copy[b];
+        cudaError_t e = enqueue_range(j, static_cast<char*>(c->scratch[b]), p0, p1);
+        if (e != cudaSuccess) return cuda_fail(e, "fill kernel launch");
+        void* dst = out_pinned ? static_cast<void*>(out + p0 * isz) : c->pinned[b];
+        BCN_CUDA(cudaMemcpyAsync(dst, c->scratch[b], (p1 - p0) * isz, cudaMemcpyDeviceToHost, c->copy[b]));
+        if (!out_pinned) {
+            // Drain the previous chunk from its staging buffer while this one copies.
+            if (k >= 1) {
+                const int pb = b ^ 1;
+                const uint64_t q0 = (k - 1) * chunk_items, q1 = std::min(n, q0 + chunk_items);
+                BCN_CUDA(cudaStreamSynchronize(c->copy[pb]));
+                std::memcpy(out + q0 * isz, c->pinned[pb], (q1 - q0) * isz);
+            }
+        }
+    }
+    BCN_CUDA(cudaStreamSynchronize(c->copy[0]));
+    BCN_CUDA(cudaStreamSynchronize(c->copy[1]));
+    if (!out_pinned && nchunks >= 1) {
+        const uint64_t k = nchunks - 1;
+        const uint64_t q0 = k * chunk_items, q1 = n;
+        std::memcpy(out + q0 * isz, c->pinned[k & 1], (q1 - q0) * isz);
+    }
+    return BCN_OK;
+}
+
+enum class PtrKind { Device, PinnedHost, PageableHost };
+
+bcn_status classify(const void* p, int* device, PtrKind* kind) {
+    cudaPointerAttributes attr;
+    cudaError_t e = cudaPointerGetAttributes(&attr, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *kind = PtrKind::PageableHost;
+        return BCN_OK;
+    }
+    switch (attr.type) {
+        case cudaMemoryTypeDevice:
+        case cudaMemoryTypeManaged:
+            if (*device < 0) *device = attr.device;
+            if (attr.device != *device)
+                return fail(BCN_ERR_INVALID_ARGUMENT, "fill: device pointer belongs to another device");
+            *kind = PtrKind::Device;
+            return BCN_OK;
+        case cudaMemoryTypeHost:
+            *kind = PtrKind::PinnedHost;
+            return BCN_OK;
+        default:
+            *kind = PtrKind::PageableHost;
+            return BCN_OK;
+    }
+}
+
+bcn_status do_fill(void* out, uint64_t capacity, uint64_t n, int fmt, uint32_t workers, int layout,
+                   uint64_t seed_index, int method, uint64_t base_offset, int engine, int device,
+                   void* stream) {
+    Plan plan;
+    bcn_status st = make_plan(n, workers, layout, &plan);
+    if (st) return st;
+    if ((st = validate_enums(fmt, layout, method, engine))) return st;
+    if (capacity < plan.n) return fail(BCN_ERR_INVALID_ARGUMENT, "fill: buffer smaller than plan.n");
+    if (!out) return fail(BCN_ERR_INVALID_ARGUMENT, "fill: null output buffer");
+    if ((st = check_seed(seed_index))) return st;
+    if (plan.n >= (1ull << 40)) return fail(BCN_ERR_INVALID_ARGUMENT, "fill: n must be below 2^40 per call");
+    const int isz = format_itemsize(fmt);
+    if (reinterpret_cast<uintptr_t>(out) % isz)
+        return fail(BCN_ERR_INVALID_ARGUMENT, "fill: buffer not aligned to its item size");
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        return fail(BCN_ERR_CUDA, "no CUDA device available (the B200 path has no CPU fallback)");
+    }
+    PtrKind kind;
+    int dev = device;
+    if ((st = classify(out, &dev, &kind))) return st;
+    if (dev < 0) dev = 0;
+    DevCtx* c = nullptr;
+    if ((st = get_ctx(dev, &c))) return st;
+    FillJob j;
+    j.plan = &plan;
+    j.fmt = fmt;
+    j.engine = resolve_engine(engine, fmt);
+    j.a = seed_index;
+    j.base_offset = base_offset;
+    j.a_exp = (seed_index - kModulus - 1) % kPeriod;
+    j.ctx = c;
+    if (kind != PtrKind::Device) return fill_host(j, static_cast<char*>(out), kind == PtrKind::PinnedHost);
+    j.stream = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+    cudaError_t e = enqueue_range(j, static_cast<char*>(out), 0, plan.n);
+    if (e != cudaSuccess) return cuda_fail(e, "fill kernel launch");
+    if (!stream) BCN_CUDA(cudaStreamSynchronize(c->stream));
+    return BCN_OK;
+}
+
+}  // namespace
+
+// ===================================================================== C ABI
+extern "C" {
+
+int bcn_abi_version(void) { return BCN_ABI_VERSION; }
+
+const char* bcn_last_error(void) { return g_last_error.c_str(); }
+
+const char* bcn_engine_name(int engine) {
+    switch (engine) {
+        case BCN_ENGINE_AUTO: return "auto";
+        case BCN_ENGINE_BARRETT: return "barrett";
+        case BCN_ENGINE_MONTGOMERY: return "montgomery";
+        case BCN_ENGINE_FP64: return "fp64";
+        case BCN_ENGINE_STAGED: return "staged";
+    }
+    return "?";
+}
+
+int bcn_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int bcn_auto_engine(bcn_format format) { return resolve_engine(kEngAuto, format); }
+
+uint64_t bcn_launch_count(void) { return launch_count(); }
+
+bcn_status bcn_modpow2(uint64_t e, uint64_t modulus, uint64_t* out) {
+    // generator.cpp:17-30
+    if (!out) return fail(BCN_ERR_INVALID_ARGUMENT, "modpow2: null output");
+    if (modulus % 2 == 0) return fail(BCN_ERR_INVALID_ARGUMENT, "modpow2: modulus must be odd");
+    if (modulus >= (1ull << 63)) return fail(BCN_ERR_INVALID_ARGUMENT, "modpow2: modulus must be below 2^63");
+    uint64_t r = 1 % modulus, b = 2 % modulus;
+    while (e) {
+        if (e & 1) r = static_cast<uint64_t>(static_cast<unsigned __int128>(r) * b % modulus);
+        b = static_cast<uint64_t>(static_cast<unsigned __int128>(b) * b % modulus);
+        e >>= 1;
+    }
+    *out = r;
+    return BCN_OK;
+}
+
+bcn_status bcn_seed_from_index(uint64_t a, uint64_t* z0) {
+    // generator.cpp:32-40
+    if (!z0) return fail(BCN_ERR_INVALID_ARGUMENT, "seed_from_index: null output");
+    bcn_status st = check_seed(a);
+    if (st) return st;
+    *z0 = host_mulmod(host_pow2(a - kModulus), kHalfM);
+    return BCN_OK;
+}
+
+bcn_status bcn_state_at(uint64_t a, uint64_t k, uint64_t* z) {
+    // generator.cpp:42-49
+    if (!z) return fail(BCN_ERR_INVALID_ARGUMENT, "state_at: null output");
+    bcn_status st = check_seed(a);
+    if (st) return st;
+    const uint64_t z0 = host_mulmod(host_pow2(a - kModulus), kHalfM);
+    *z = host_mulmod(host_pow2(host_mul53_mod_p(k)), z0);
+    return BCN_OK;
+}
+
+bcn_status bcn_next(uint64_t* z) {
+    // generator.hpp:52-70 (all methods agree; modred.hpp:150 rejects z = 0)
+    if (!z) return fail(BCN_ERR_INVALID_ARGUMENT, "next: null state");
+    if (*z == 0) return fail(BCN_ERR_DOMAIN, "barrett_modified_step: z = 0 not in domain");
+    if (*z >= kModulus) return fail(BCN_ERR_DOMAIN, "barrett_modified_step: residue out of range");
+    *z = static_cast<uint64_t>((static_cast<unsigned __int128>(*z) << 53) % kModulus);
+    return BCN_OK;
+}
+
+bcn_status bcn_to_unit_interval(uint64_t z, double* u) {
+    // generator.hpp:74-78
+    if (!u) return fail(BCN_ERR_INVALID_ARGUMENT, "to_unit_interval: null output");
+    if (z == 0) return fail(BCN_ERR_DOMAIN, "to_unit_interval: z = 0 maps outside (0,1)");
+    if (z >= kModulus) return fail(BCN_ERR_DOMAIN, "to_unit_interval: residue out of range");
+    *u = static_cast<double>(z) * kInvModulus;
+    return BCN_OK;
+}
+
+bcn_status bcn_make_plan(uint64_t n, uint32_t workers, uint32_t* eff_workers,
+                         uint64_t* work_per_worker) {
+    Plan p;
+    bcn_status st = make_plan(n, workers, 0, &p);
+    if (st) return st;
+    if (eff_workers) *eff_workers = p.workers;
+    if (work_per_worker) *work_per_worker = p.wpw;
+    return BCN_OK;
+}
+
+bcn_status bcn_physical_index(uint64_t n, uint32_t workers, bcn_layout layout, uint32_t w,
+                              uint64_t i, uint64_t* slot) {
+    Plan p;
+    bcn_status st = make_plan(n, workers, layout, &p);
+    if (st) return st;
+    if (!slot) return fail(BCN_ERR_INVALID_ARGUMENT, "physical_index: null output");
+    if (w >= p.workers || i >= p.elements_for(w))
+        return fail(BCN_ERR_INVALID_ARGUMENT, "physical_index: (w, i) outside the plan");
+    if (layout == BCN_LAYOUT_CONTIGUOUS) {
+        *slot = static_cast<uint64_t>(w) * p.wpw + i;
+    } else {
+        const uint64_t sc = p.short_count();
+        *slot = i < sc ? i * p.workers + w : sc * p.workers + (i - sc) * (p.workers - 1) + w;
+    }
+    return BCN_OK;
+}
+
+bcn_status bcn_fill(void* out, uint64_t capacity, uint64_t n, bcn_format format, uint32_t workers,
+                    bcn_layout layout, uint64_t seed_index, bcn_method method, uint64_t base_offset,
+                    bcn_engine engine, int device, void* stream) {
+    return do_fill(out, capacity, n, format, workers, layout, seed_index, method, base_offset,
+                   engine, device, stream);
+}
+
+bcn_status bcn_fill_multi(void* const* outs, const int* devices, int ndev, uint64_t n,
+                          bcn_format format, uint64_t seed_index, uint64_t base_offset,
+                          bcn_engine engine) {
+    if (!outs || !devices || ndev <= 0) return fail(BCN_ERR_INVALID_ARGUMENT, "fill_multi: no devices");
+    Plan plan;
+    bcn_status st = make_plan(n, static_cast<uint32_t>(ndev), 0, &plan);
+    if (st) return st;
+    if ((st = validate_enums(format, 0, 3, engine))) return st;
+    if ((st = check_seed(seed_index))) return st;
+    std::vector<bcn_status> res(plan.workers, BCN_OK);
+    std::vector<std::string> msg(plan.workers);
+    std::vector<std::thread> pool;
+    for (uint32_t g = 0; g < plan.workers; ++g) {
+        pool.emplace_back([&, g] {
+            DevCtx* c = nullptr;
+            bcn_status s = get_ctx(devices[g], &c);
+            if (!s) {
+                FillJob j;
+                j.plan = &plan;
+                j.fmt = format;
+                j.engine = resolve_engine(engine, format);
+                j.a = seed_index;
+                j.base_offset = base_offset;
+                j.a_exp = (seed_index - kModulus - 1) % kPeriod;
+                j.ctx = c;
+                j.stream = c->stream;
+                const uint64_t p0 = static_cast<uint64_t>(g) * plan.wpw;
+                cudaError_t e = enqueue_range(j, static_cast<char*>(outs[g]), p0, p0 + plan.elements_for(g));
+                if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+                if (e != cudaSuccess) s = cuda_fail(e, "fill_multi shard");
+            }
+            res[g] = s;
+            msg[g] = g_last_error;
+        });
+    }
+    for (auto& t : pool) t.join();
+    for (uint32_t g = 0; g < plan.workers; ++g)
+        if (res[g]) return fail(res[g], "device " + std::to_string(devices[g]) + ": " + msg[g]);
+    return BCN_OK;
+}
+
+bcn_status bcn_deinterleave(const void* in, void* out, uint64_t n, uint32_t workers,
+                            uint32_t itemsize, int device, void* stream) {
+    Plan p;
+    bcn_status st = make_plan(n, workers, 1, &p);
+    if (st) return st;
+    if (!in || !out) return fail(BCN_ERR_INVALID_ARGUMENT, "deinterleave: null buffer");
+    if (itemsize != 4 && itemsize != 8) return fail(BCN_ERR_INVALID_ARGUMENT, "deinterleave: itemsize must be 4 or 8");
+    PtrKind kin, kout;
+    int dev = device;
+    if ((st = classify(in, &dev, &kin))) return st;
+    if ((st = classify(out, &dev, &kout))) return st;
+    if ((kin == PtrKind::Device) != (kout == PtrKind::Device))
+        return fail(BCN_ERR_INVALID_ARGUMENT, "deinterleave: mixed host/device buffers");
+    if (dev < 0) dev = 0;
+    DevCtx* c = nullptr;
+    if ((st = get_ctx(dev, &c))) return st;
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+    const void* din = in;
+    void* dout = out;
+    void* tmp = nullptr;
+    const size_t bytes = n * itemsize;
+    if (kin != PtrKind::Device) {
+        BCN_CUDA(cudaMalloc(&tmp, 2 * bytes));
+        BCN_CUDA(cudaMemcpyAsync(tmp, in, bytes, cudaMemcpyHostToDevice, s));
+        din = tmp;
+        dout = static_cast<char*>(tmp) + bytes;
+    }
+    const uint64_t sc = p.short_count();
+    TransposeArgs t;
+    t.in = din;
+    t.out = dout;
+    t.wpw = p.wpw;
+    t.itemsize = itemsize;
+    // Region 1: rows [0, sc) of all workers; region 2: the remaining
+    // wpw - sc elements of workers 0..W-2 (parallel.cpp:24-33). Rows are
+    // processed in launches of at most 65535*32.
+    for (int region = 0; region < 2; ++region) {
+        const uint64_t rows = region == 0 ? sc : p.wpw - sc;
+        const uint64_t width = region == 0 ? p.workers : p.workers - 1;
+        const uint64_t p0 = region == 0 ? 0 : sc * p.workers;
+        const uint64_t ib = region == 0 ? 0 : sc;
+        if (rows == 0 || width == 0) continue;
+        const uint64_t max_rows = 65535ull * 32;
+        for (uint64_t r0 = 0; r0 < rows; r0 += max_rows) {
+            t.p0 = p0 + r0 * width;
+            t.rows = std::min(max_rows, rows - r0);
+            t.width = width;
+            t.i_base = ib + r0;
+            cudaError_t e = launch_transpose(t, s);
+            if (e != cudaSuccess) return cuda_fail(e, "deinterleave launch");
+        }
+    }
+    if (tmp) {
+        BCN_CUDA(cudaMemcpyAsync(out, dout, bytes, cudaMemcpyDeviceToHost, s));
+        BCN_CUDA(cudaStreamSynchronize(s));
+        cudaFree(tmp);
+    } else if (!stream) {
+        BCN_CUDA(cudaStreamSynchronize(s));
+    }
+    return BCN_OK;
+}
+
+bcn_status bcn_seed_states(const uint64_t* a, const uint64_t* k, uint64_t* out, uint64_t count,
+                           uint32_t steps, int device, void* stream) {
+    if (!a || !k || !out) return fail(BCN_ERR_INVALID_ARGUMENT, "seed_states: null buffer");
+    if (count == 0) return BCN_OK;
+    int dev = device;
+    PtrKind kind;
+    bcn_status st = classify(out, &dev, &kind);
+    if (st) return st;
+    if (kind != PtrKind::Device) return fail(BCN_ERR_INVALID_ARGUMENT, "seed_states: buffers must be device memory");
+    DevCtx* c = nullptr;
+    if ((st = get_ctx(dev, &c))) return st;
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+    BCN_CUDA(cudaMemsetAsync(c->flag, 0, sizeof(int), s));
+    SeedArgs sa{a, k, out, count, steps, c->flag};
+    cudaError_t e = launch_seed(sa, s);
+    if (e != cudaSuccess) return cuda_fail(e, "seed_states launch");
+    int flag = 0;
+    BCN_CUDA(cudaMemcpyAsync(&flag, c->flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    BCN_CUDA(cudaStreamSynchronize(s));
+    if (flag) return fail(BCN_ERR_OUT_OF_RANGE, "seed_from_index: index outside [3^33+100, 2^53]");
+    return BCN_OK;
+}
+
+bcn_status bcn_digest(const void* buf, uint64_t n, uint32_t itemsize, uint64_t index_base,
+                      uint64_t d[3], int device, void* stream) {
+    if (!buf || !d) return fail(BCN_ERR_INVALID_ARGUMENT, "digest: null buffer");
+    if (itemsize != 4 && itemsize != 8) return fail(BCN_ERR_INVALID_ARGUMENT, "digest: itemsize must be 4 or 8");
+    int dev = device;
+    PtrKind kind;
+    bcn_status st = classify(buf, &dev, &kind);
+    if (st) return st;
+    if (kind != PtrKind::Device) return fail(BCN_ERR_INVALID_ARGUMENT, "digest: buffer must be device memory");
+    DevCtx* c = nullptr;
+    if ((st = get_ctx(dev, &c))) return st;
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+    BCN_CUDA(cudaMemsetAsync(c->digest, 0, 3 * sizeof(unsigned long long), s));
+    DigestArgs da{buf, n, itemsize, index_base, c->digest};
+    if (n) {
+        const int grid = static_cast<int>(std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(c->sms) * 8));
+        cudaError_t e = launch_digest(da, grid, s);
+        if (e != cudaSuccess) return cuda_fail(e, "digest launch");
+    }
+    unsigned long long h[3];
+    BCN_CUDA(cudaMemcpyAsync(h, c->digest, sizeof(h), cudaMemcpyDeviceToHost, s));
+    BCN_CUDA(cudaStreamSynchronize(s));
+    for (int i = 0; i < 3; ++i) d[i] = h[i];
+    return BCN_OK;
+}
+
+bcn_status bcn_fill_constant(void* out, uint64_t nbytes, uint64_t pattern, int device, void* stream) {
+    if (!out) return fail(BCN_ERR_INVALID_ARGUMENT, "fill_constant: null buffer");
+    if (reinterpret_cast<uintptr_t>(out) % 32 || nbytes % 1024)
+        return fail(BCN_ERR_INVALID_ARGUMENT, "fill_constant: needs 32-byte alignment and whole 1 KiB rows");
+    int dev = device;
+    PtrKind kind;
+    bcn_status st = classify(out, &dev, &kind);
+    if (st) return st;
+    if (kind != PtrKind::Device) return fail(BCN_ERR_INVALID_ARGUMENT, "fill_constant: buffer must be device memory");
+    DevCtx* c = nullptr;
+    if ((st = get_ctx(dev, &c))) return st;
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+    ConstArgs ca{out, nbytes / 1024, pattern};
+    const int grid = grid_for_rows(c, kFmtF64, kEngBarrett, false, ca.rows);
+    cudaError_t e = launch_constant(ca, grid, kContigThreads, s);
+    if (e != cudaSuccess) return cuda_fail(e, "fill_constant launch");
+    if (!stream) BCN_CUDA(cudaStreamSynchronize(s));
+    return BCN_OK;
+}
+
+}  // extern "C"

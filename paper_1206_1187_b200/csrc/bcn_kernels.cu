@@ -1,0 +1,627 @@
+// bcn_kernels.cu — sm_100a kernels for the alpha_{2,3} generator fill path.
+//
+// Kernel inventory:
+//   k_fill_contig<FMT, ENG>       logical-order fill, lane-interleaved jump streams,
+//                                 256-bit stores (STG.E.256), persistent grid.
+//   k_fill_interleaved<FMT, ENG>  reference Layout::Interleaved, same machinery
+//                                 with a per-stream row-crossing multiplier select.
+//   k_fill_staged<FMT>            the paper's T=1 modified-Barrett step per thread,
+//                                 tile staged in smem, TMA bulk store per tile.
+//   k_fill_slots<FMT>             exact per-slot reference semantics (head/tail,
+//                                 u64-wrap corner cases); one seed per slot.
+//   k_seed                        batched state_at / next walks (skip-ahead stress).
+//   k_digest                      order-sensitive checksums for verification.
+//   k_constant                    the Constant writer: identical access pattern,
+//                                 fixed value (the paper's memory ceiling).
+//   k_transpose                   device deinterleave (Interleaved -> logical).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <atomic>
+#include <mutex>
+
+#include "bcn_kernels.cuh"
+
+namespace bcn_b200 {
+
+// --------------------------------------------------------------- seed tables
+// g_pow[i][d] = {2^(d 16^i) mod m, Shoup(...)} for 13 4-bit windows.
+__device__ uint64_t g_pow[kPowWindows][16][2];
+
+// 2^E mod m for E < P: 13 table multiplies (12 Barrett/Shoup products).
+__device__ __forceinline__ uint64_t dev_pow2(uint64_t e) {
+    uint64_t acc = __ldg(&g_pow[0][e & 15][0]);
+    e >>= 4;
+#pragma unroll
+    for (int i = 1; i < kPowWindows; ++i) {
+        const unsigned d = static_cast<unsigned>(e & 15);
+        e >>= 4;
+        acc = mul_barrett(acc, __ldg(&g_pow[i][d][0]), __ldg(&g_pow[i][d][1]));
+    }
+    return acc;
+}
+
+// Canonical state with 2-exponent E: z = m - (2^E mod m), never 0.
+__device__ __forceinline__ uint64_t dev_state_from_exp(uint64_t e) {
+    return kModulus - dev_pow2(e);
+}
+
+// (e0 + 53 j) mod P for e0 < P and j < 2^40 (53 j < 2^46 < P).
+__device__ __forceinline__ uint64_t dev_exp_at(uint64_t e0, uint64_t j) {
+    uint64_t e = e0 + 53ull * j;
+    return e >= kPeriod ? e - kPeriod : e;
+}
+
+// ------------------------------------------------------------------ engines
+template <int ENG>
+struct Eng;
+
+template <>
+struct Eng<kEngBarrett> {
+    using State = uint64_t;
+    static __device__ __forceinline__ State from_canonical(uint64_t z) { return z; }
+    static __device__ __forceinline__ State mul(State s, const Mult& k) {
+        return mul_barrett(s, k.c, k.shoup);
+    }
+    static __device__ __forceinline__ uint64_t raw(State s) { return s; }
+    static __device__ __forceinline__ double unit(State s) { return unit_from_u64(s); }
+};
+
+template <>
+struct Eng<kEngMontgomery> {
+    using State = uint64_t;
+    static __device__ __forceinline__ State from_canonical(uint64_t z) { return z; }
+    static __device__ __forceinline__ State mul(State s, const Mult& k) {
+        return mul_montgomery(s, k.mont);
+    }
+    static __device__ __forceinline__ uint64_t raw(State s) { return s; }
+    static __device__ __forceinline__ double unit(State s) { return unit_from_u64(s); }
+};
+
+template <>
+struct Eng<kEngFP64> {
+    using State = double;  // balanced residue, |s| <= 0.75 m, integer valued
+    static __device__ __forceinline__ State from_canonical(uint64_t z) {
+        return z > kModulus / 2 ? static_cast<double>(static_cast<int64_t>(z - kModulus))
+                                : static_cast<double>(z);
+    }
+    static __device__ __forceinline__ State mul(State s, const Mult& k) {
+        return mul_fp64(s, k.cb, k.com);
+    }
+    static __device__ __forceinline__ uint64_t raw(State s) {
+        return __double2ull_rz(fp64_canonical(s));
+    }
+    static __device__ __forceinline__ double unit(State s) {
+        return __dmul_rn(fp64_canonical(s), kInvModulus);
+    }
+};
+
+// --------------------------------------------------------------- formats
+template <int FMT>
+struct Fmt;
+template <>
+struct Fmt<kFmtU64> {
+    static constexpr int kVec = 4;  // 4 x 8 B = one 256-bit store per lane
+    using Item = uint64_t;
+};
+template <>
+struct Fmt<kFmtF64> {
+    static constexpr int kVec = 4;
+    using Item = double;
+};
+template <>
+struct Fmt<kFmtF32> {
+    static constexpr int kVec = 8;  // 8 x 4 B
+    using Item = float;
+};
+
+template <int FMT, class E>
+__device__ __forceinline__ uint64_t emit_bits(typename E::State s) {
+    if constexpr (FMT == kFmtU64) {
+        return E::raw(s);
+    } else if constexpr (FMT == kFmtF64) {
+        return static_cast<uint64_t>(__double_as_longlong(E::unit(s)));
+    } else {
+        return static_cast<uint64_t>(__float_as_uint(f32_rz_from_unit(E::unit(s))));
+    }
+}
+
+// 32-byte store: st.global.v4.b64 / v8.b32 -> SASS STG.E.256 on sm_100a.
+__device__ __forceinline__ void st256(void* p, const uint64_t (&v)[4]) {
+    asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(v[0]), "l"(v[1]),
+                 "l"(v[2]), "l"(v[3])
+                 : "memory");
+}
+
+template <int FMT>
+__device__ __forceinline__ void pack_store(void* p, const uint64_t (&bits)[Fmt<FMT>::kVec]) {
+    uint64_t w[4];
+    if constexpr (Fmt<FMT>::kVec == 4) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) w[i] = bits[i];
+    } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) w[i] = bits[2 * i] | (bits[2 * i + 1] << 32);
+    }
+    st256(p, w);
+}
+
+// Splits `rows` over `nw` warps: warp w gets [begin, end).
+__device__ __forceinline__ void warp_rows(uint64_t rows, uint64_t nw, uint64_t w, uint64_t& begin,
+                                          uint64_t& end) {
+    const uint64_t q = rows / nw, r = rows % nw;
+    begin = w * q + (w < r ? w : r);
+    end = begin + q + (w < r ? 1 : 0);
+}
+
+// ---------------------------------------------------------- contiguous fill
+// A "row" is 32 lanes x kVec consecutive elements (1 KiB). Lane l holds kVec
+// independent streams at elements row*ROW + l*kVec + v; every row each stream
+// is multiplied by 2^(53 ROW) mod m. Consecutive lanes store consecutive
+// 32-byte sectors, so every warp store is one fully coalesced 1 KiB write.
+template <int FMT, int ENG>
+__global__ void __launch_bounds__(kContigThreads) k_fill_contig(const ContigArgs a) {
+    using E = Eng<ENG>;
+    constexpr int V = Fmt<FMT>::kVec;
+    constexpr uint64_t ROW = 32ull * V;
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
+    const uint64_t w = static_cast<uint64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    uint64_t r, r_end;
+    warp_rows(a.rows, nw, w, r, r_end);
+    if (r >= r_end) return;
+
+    // Seed: one windowed power per lane, then T=1 steps for the lane's vector.
+    typename E::State st[V];
+    {
+        uint64_t z = dev_state_from_exp(dev_exp_at(a.e0, r * ROW + lane * V));
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            st[v] = E::from_canonical(z);
+            if (v + 1 < V) z = step_modified_barrett(z);
+        }
+    }
+    const Mult k = a.jump_row;
+    char* p = static_cast<char*>(a.out) + (r * ROW + lane * V) * sizeof(typename Fmt<FMT>::Item);
+    constexpr uint64_t kRowBytes = ROW * sizeof(typename Fmt<FMT>::Item);
+#pragma unroll 2
+    for (; r < r_end; ++r) {
+        uint64_t bits[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) bits[v] = emit_bits<FMT, E>(st[v]);
+        pack_store<FMT>(p, bits);
+#pragma unroll
+        for (int v = 0; v < V; ++v) st[v] = E::mul(st[v], k);
+        p += kRowBytes;
+    }
+}
+
+// -------------------------------------------------------- interleaved fill
+template <int FMT, int ENG>
+__global__ void __launch_bounds__(kContigThreads) k_fill_interleaved(const InterleavedArgs a) {
+    using E = Eng<ENG>;
+    constexpr int V = Fmt<FMT>::kVec;
+    constexpr uint64_t ROW = 32ull * V;
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
+    const uint64_t w = static_cast<uint64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    uint64_t r, r_end;
+    warp_rows(a.rows, nw, w, r, r_end);
+    if (r >= r_end) return;
+
+    typename E::State st[V];
+    uint64_t col[V];  // worker index of each stream's current slot
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+        const uint64_t q = a.q0 + r * ROW + lane * V + v;
+        col[v] = q % a.width;
+        const uint64_t j = col[v] * a.wpw + a.i_base + q / a.width;
+        st[v] = E::from_canonical(dev_state_from_exp(dev_exp_at(a.e0, j)));
+    }
+    char* p = static_cast<char*>(a.out) + (r * ROW + lane * V) * sizeof(typename Fmt<FMT>::Item);
+    constexpr uint64_t kRowBytes = ROW * sizeof(typename Fmt<FMT>::Item);
+    for (; r < r_end; ++r) {
+        uint64_t bits[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) bits[v] = emit_bits<FMT, E>(st[v]);
+        pack_store<FMT>(p, bits);
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            const bool same = col[v] + a.adv_b < a.width;
+            st[v] = E::mul(st[v], same ? a.jump_same : a.jump_wrap);
+            col[v] = same ? col[v] + a.adv_b : col[v] + a.adv_b - a.width;
+        }
+        p += kRowBytes;
+    }
+}
+
+// ------------------------------------------------------------- slot fill
+// Exact reference semantics for arbitrary slots: physical slot p -> (w, i)
+// (parallel.cpp:24-33) -> state after i+1 steps from state_at(a, B + start_w)
+// with B + start_w wrapping mod 2^64 exactly as the reference's u64 does.
+__device__ __forceinline__ void slot_to_worker(const SlotArgs& a, uint64_t p, uint64_t& w,
+                                               uint64_t& i) {
+    if (a.layout == 0) {
+        w = p / a.wpw;
+        i = p % a.wpw;
+        return;
+    }
+    const uint64_t last_start = static_cast<uint64_t>(a.workers - 1) * a.wpw;
+    const uint64_t short_count = a.n - last_start < a.wpw ? a.n - last_start : a.wpw;
+    const uint64_t main = short_count * a.workers;
+    if (p < main) {
+        w = p % a.workers;
+        i = p / a.workers;
+    } else {
+        const uint64_t q = p - main, width = a.workers - 1;
+        w = q % width;
+        i = short_count + q / width;
+    }
+}
+
+template <int FMT>
+__global__ void __launch_bounds__(128) k_fill_slots(const SlotArgs a) {
+    const uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= a.count) return;
+    uint64_t w, i;
+    slot_to_worker(a, a.slot0 + t, w, i);
+    const uint64_t kw = a.base_offset + w * a.wpw;  // wraps mod 2^64 like the reference
+    const uint64_t steps = (kw % kPeriod + (i % kPeriod) + 1) % kPeriod;
+    const uint64_t e = (a.a_exp + (53ull * steps) % kPeriod) % kPeriod;
+    const uint64_t z = dev_state_from_exp(e);
+    using Item = typename Fmt<FMT>::Item;
+    Item* out = static_cast<Item*>(a.out) + t;
+    if constexpr (FMT == kFmtU64) {
+        *out = z;
+    } else if constexpr (FMT == kFmtF64) {
+        *out = unit_from_u64(z);
+    } else {
+        *out = f32_rz_from_unit(unit_from_u64(z));
+    }
+}
+
+// ----------------------------------------------------------- staged (TMA)
+// The paper's design (Fig. 3/4): each thread advances its own
+// logically contiguous run with the T=1 modified Barrett step. Runs are
+// written to shared memory at their logical positions (stride L words, L odd
+// => conflict-free) and the whole tile leaves with ONE cp.async.bulk
+// (TMA bulk store, SASS UBLKCP) issued by one thread; two tiles in flight.
+template <int FMT>
+__global__ void __launch_bounds__(kStagedThreads) k_fill_staged(const StagedArgs a) {
+    using Item = typename Fmt<FMT>::Item;
+    constexpr int L = kStagedL;
+    constexpr uint32_t TILE = kStagedThreads * L;
+    constexpr uint32_t TILE_BYTES = TILE * sizeof(Item);
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const unsigned tid = threadIdx.x;
+    uint64_t tile = blockIdx.x;
+    if (tile >= a.tiles) return;
+    uint64_t z = dev_state_from_exp(dev_exp_at(a.e0, tile * TILE + tid * L));
+    int b = 0;
+    for (; tile < a.tiles; tile += gridDim.x, b ^= 1) {
+        if (tid == 0) {
+            // The bulk store issued two tiles ago read from this buffer.
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        }
+        __syncthreads();
+        Item* const tile_buf = reinterpret_cast<Item*>(smem_raw + b * TILE_BYTES);
+        Item* t = tile_buf + tid * L;
+#pragma unroll
+        for (int i = 0; i < L; ++i) {
+            if constexpr (FMT == kFmtU64) {
+                t[i] = z;
+            } else if constexpr (FMT == kFmtF64) {
+                t[i] = unit_from_u64(z);
+            } else {
+                t[i] = f32_rz_from_unit(unit_from_u64(z));
+            }
+            z = step_modified_barrett(z);
+        }
+        // Make generic-proxy smem writes visible to the async (TMA) proxy.
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (tid == 0) {
+            const uint32_t src = static_cast<uint32_t>(__cvta_generic_to_shared(tile_buf));
+            char* dst = static_cast<char*>(a.out) + tile * TILE_BYTES;
+            asm volatile(
+                "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n\t"
+                "cp.async.bulk.commit_group;" ::"l"(dst),
+                "r"(src), "r"(TILE_BYTES)
+                : "memory");
+        }
+        z = mul_barrett(z, a.jump_next.c, a.jump_next.shoup);
+    }
+    if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// -------------------------------------------------------- seed / walks
+// SeedArgs.steps == 0: out[t] = state_at(a[t], k[t]) (generator.cpp:42-49).
+// steps > 0: out[t*steps + s] = the (s+1)-th next() from that state.
+__global__ void __launch_bounds__(256) k_seed(const SeedArgs a) {
+    const uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= a.count) return;
+    const uint64_t idx = a.a[t];
+    if (idx < kMinSeed || idx > kMaxSeed) {
+        *a.error = 1;
+        return;
+    }
+    const uint64_t ae = (idx - kModulus - 1) % kPeriod;
+    const uint64_t e = (ae + (53ull * (a.k[t] % kPeriod)) % kPeriod) % kPeriod;
+    uint64_t z = dev_state_from_exp(e);
+    if (a.steps == 0) {
+        a.out[t] = z;
+        return;
+    }
+    uint64_t* o = a.out + t * a.steps;
+    for (uint32_t s = 0; s < a.steps; ++s) {
+        z = step_modified_barrett(z);
+        o[s] = z;
+    }
+}
+
+// ------------------------------------------------------------- digest
+__global__ void __launch_bounds__(256) k_digest(const DigestArgs a) {
+    unsigned long long s = 0, ws = 0, x = 0;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < a.n;
+         i += stride) {
+        const uint64_t v = a.itemsize == 8 ? static_cast<const uint64_t*>(a.buf)[i]
+                                           : static_cast<const uint32_t*>(a.buf)[i];
+        const uint64_t g = i + a.index_base;
+        s += v;
+        ws += (g + 1) * v;
+        x ^= v * (2 * g + 1);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+        ws += __shfl_xor_sync(0xffffffffu, ws, o);
+        x ^= __shfl_xor_sync(0xffffffffu, x, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&a.out[0], s);
+        atomicAdd(&a.out[1], ws);
+        atomicXor(&a.out[2], x);
+    }
+}
+
+// ------------------------------------------------------------- constant
+// The reference's Constant baseline (bench.cpp:60-63): the same
+// rows-per-warp split and 256-bit lane stores as k_fill_contig, fixed value.
+__global__ void __launch_bounds__(kContigThreads) k_constant(const ConstArgs a) {
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
+    const uint64_t w = static_cast<uint64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    uint64_t r, r_end;
+    warp_rows(a.rows, nw, w, r, r_end);
+    const uint64_t v[4] = {a.value, a.value, a.value, a.value};
+    char* p = static_cast<char*>(a.out) + r * 1024 + lane * 32;
+#pragma unroll 4
+    for (; r < r_end; ++r, p += 1024) st256(p, v);
+}
+
+// ------------------------------------------------------------ transpose
+// Device deinterleave of one Interleaved region: the region is a row-major
+// [rows x width] matrix M[i][w] at physical slot p0; logical position of
+// M[i][w] is w*wpw + i_base + i. 32x32 smem tiles keep both sides coalesced.
+template <typename T>
+__global__ void __launch_bounds__(256) k_transpose(const TransposeArgs a) {
+    __shared__ T tile[32][33];
+    const T* in = static_cast<const T*>(a.in);
+    T* out = static_cast<T*>(a.out);
+    const uint64_t i0 = static_cast<uint64_t>(blockIdx.y) * 32;  // region row (element)
+    const uint64_t w0 = static_cast<uint64_t>(blockIdx.x) * 32;  // worker
+    for (int dy = threadIdx.y; dy < 32; dy += 8) {
+        const uint64_t i = i0 + dy, w = w0 + threadIdx.x;
+        if (i < a.rows && w < a.width) tile[dy][threadIdx.x] = in[a.p0 + i * a.width + w];
+    }
+    __syncthreads();
+    for (int dy = threadIdx.y; dy < 32; dy += 8) {
+        const uint64_t w = w0 + dy, i = i0 + threadIdx.x;
+        if (i < a.rows && w < a.width) out[w * a.wpw + a.i_base + i] = tile[threadIdx.x][dy];
+    }
+}
+
+// ============================================================ launchers
+std::atomic<uint64_t> g_launches{0};
+
+uint64_t launch_count() { return g_launches.load(); }
+
+namespace {
+
+cudaError_t counted(cudaError_t e) {
+    if (e == cudaSuccess) g_launches.fetch_add(1);
+    return e;
+}
+
+template <int FMT>
+cudaError_t contig_fmt(int engine, const ContigArgs& a, int grid, int block, cudaStream_t s) {
+    switch (engine) {
+        case kEngBarrett:
+            k_fill_contig<FMT, kEngBarrett><<<grid, block, 0, s>>>(a);
+            break;
+        case kEngMontgomery:
+            k_fill_contig<FMT, kEngMontgomery><<<grid, block, 0, s>>>(a);
+            break;
+        case kEngFP64:
+            k_fill_contig<FMT, kEngFP64><<<grid, block, 0, s>>>(a);
+            break;
+        default:
+            return cudaErrorInvalidValue;
+    }
+    return counted(cudaGetLastError());
+}
+
+template <int FMT>
+cudaError_t inter_fmt(int engine, const InterleavedArgs& a, int grid, int block, cudaStream_t s) {
+    switch (engine) {
+        case kEngBarrett:
+            k_fill_interleaved<FMT, kEngBarrett><<<grid, block, 0, s>>>(a);
+            break;
+        case kEngMontgomery:
+            k_fill_interleaved<FMT, kEngMontgomery><<<grid, block, 0, s>>>(a);
+            break;
+        case kEngFP64:
+            k_fill_interleaved<FMT, kEngFP64><<<grid, block, 0, s>>>(a);
+            break;
+        default:
+            return cudaErrorInvalidValue;
+    }
+    return counted(cudaGetLastError());
+}
+
+template <class K>
+int occupancy(K kernel, int block, size_t smem = 0) {
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, block, smem) != cudaSuccess) n = 1;
+    return n > 0 ? n : 1;
+}
+
+}  // namespace
+
+cudaError_t launch_contig(int fmt, int engine, const ContigArgs& a, int grid, int block,
+                          cudaStream_t s) {
+    switch (fmt) {
+        case kFmtU64: return contig_fmt<kFmtU64>(engine, a, grid, block, s);
+        case kFmtF64: return contig_fmt<kFmtF64>(engine, a, grid, block, s);
+        case kFmtF32: return contig_fmt<kFmtF32>(engine, a, grid, block, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_interleaved(int fmt, int engine, const InterleavedArgs& a, int grid, int block,
+                               cudaStream_t s) {
+    switch (fmt) {
+        case kFmtU64: return inter_fmt<kFmtU64>(engine, a, grid, block, s);
+        case kFmtF64: return inter_fmt<kFmtF64>(engine, a, grid, block, s);
+        case kFmtF32: return inter_fmt<kFmtF32>(engine, a, grid, block, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_slots(int fmt, const SlotArgs& a, cudaStream_t s) {
+    if (a.count == 0) return cudaSuccess;
+    const unsigned grid = static_cast<unsigned>((a.count + 127) / 128);
+    switch (fmt) {
+        case kFmtU64: k_fill_slots<kFmtU64><<<grid, 128, 0, s>>>(a); break;
+        case kFmtF64: k_fill_slots<kFmtF64><<<grid, 128, 0, s>>>(a); break;
+        case kFmtF32: k_fill_slots<kFmtF32><<<grid, 128, 0, s>>>(a); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return counted(cudaGetLastError());
+}
+
+cudaError_t launch_staged(int fmt, const StagedArgs& a, int grid, cudaStream_t s) {
+    const size_t smem = 2ull * kStagedThreads * kStagedL * format_itemsize(fmt);
+    switch (fmt) {
+        case kFmtU64:
+            cudaFuncSetAttribute(k_fill_staged<kFmtU64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem));
+            k_fill_staged<kFmtU64><<<grid, kStagedThreads, smem, s>>>(a);
+            break;
+        case kFmtF64:
+            cudaFuncSetAttribute(k_fill_staged<kFmtF64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem));
+            k_fill_staged<kFmtF64><<<grid, kStagedThreads, smem, s>>>(a);
+            break;
+        case kFmtF32:
+            cudaFuncSetAttribute(k_fill_staged<kFmtF32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem));
+            k_fill_staged<kFmtF32><<<grid, kStagedThreads, smem, s>>>(a);
+            break;
+        default:
+            return cudaErrorInvalidValue;
+    }
+    return counted(cudaGetLastError());
+}
+
+cudaError_t launch_seed(const SeedArgs& a, cudaStream_t s) {
+    if (a.count == 0) return cudaSuccess;
+    k_seed<<<static_cast<unsigned>((a.count + 255) / 256), 256, 0, s>>>(a);
+    return counted(cudaGetLastError());
+}
+
+cudaError_t launch_digest(const DigestArgs& a, int grid, cudaStream_t s) {
+    k_digest<<<grid, 256, 0, s>>>(a);
+    return counted(cudaGetLastError());
+}
+
+cudaError_t launch_constant(const ConstArgs& a, int grid, int block, cudaStream_t s) {
+    k_constant<<<grid, block, 0, s>>>(a);
+    return counted(cudaGetLastError());
+}
+
+cudaError_t launch_transpose(const TransposeArgs& a, cudaStream_t s) {
+    if (a.rows == 0 || a.width == 0) return cudaSuccess;
+    const dim3 grid(static_cast<unsigned>((a.width + 31) / 32), static_cast<unsigned>((a.rows + 31) / 32));
+    if (grid.y > 65535u) return cudaErrorInvalidValue;
+    const dim3 block(32, 8);
+    if (a.itemsize == 8) {
+        k_transpose<uint64_t><<<grid, block, 0, s>>>(a);
+    } else {
+        k_transpose<uint32_t><<<grid, block, 0, s>>>(a);
+    }
+    return counted(cudaGetLastError());
+}
+
+int contig_blocks_per_sm(int fmt, int engine, int block) {
+#define BCN_OCC(F)                                                                   \
+    switch (engine) {                                                                \
+        case kEngBarrett: return occupancy(k_fill_contig<F, kEngBarrett>, block);    \
+        case kEngMontgomery: return occupancy(k_fill_contig<F, kEngMontgomery>, block); \
+        case kEngFP64: return occupancy(k_fill_contig<F, kEngFP64>, block);          \
+    }
+    switch (fmt) {
+        case kFmtU64: BCN_OCC(kFmtU64) break;
+        case kFmtF64: BCN_OCC(kFmtF64) break;
+        case kFmtF32: BCN_OCC(kFmtF32) break;
+    }
+#undef BCN_OCC
+    return 1;
+}
+
+int interleaved_blocks_per_sm(int fmt, int engine, int block) {
+#define BCN_OCC(F)                                                                        \
+    switch (engine) {                                                                     \
+        case kEngBarrett: return occupancy(k_fill_interleaved<F, kEngBarrett>, block);    \
+        case kEngMontgomery: return occupancy(k_fill_interleaved<F, kEngMontgomery>, block); \
+        case kEngFP64: return occupancy(k_fill_interleaved<F, kEngFP64>, block);          \
+    }
+    switch (fmt) {
+        case kFmtU64: BCN_OCC(kFmtU64) break;
+        case kFmtF64: BCN_OCC(kFmtF64) break;
+        case kFmtF32: BCN_OCC(kFmtF32) break;
+    }
+#undef BCN_OCC
+    return 1;
+}
+
+cudaError_t upload_tables() {
+    static std::mutex mu;
+    static bool done[64] = {};
+    int dev = 0;
+    cudaError_t err = cudaGetDevice(&dev);
+    if (err != cudaSuccess) return err;
+    std::lock_guard<std::mutex> lock(mu);
+    if (dev >= 0 && dev < 64 && done[dev]) return cudaSuccess;
+    static uint64_t host_tab[kPowWindows][16][2];
+    static bool built = false;
+    if (!built) {
+        for (int i = 0; i < kPowWindows; ++i) {
+            // 2^(16^i) mod m, then its powers d = 0..15.
+            const uint64_t base = host_pow2(static_cast<uint64_t>(1) << (4 * i));
+            uint64_t v = 1;
+            for (int d = 0; d < 16; ++d) {
+                host_tab[i][d][0] = v;
+                host_tab[i][d][1] = host_shoup(v);
+                v = host_mulmod(v, base);
+            }
+        }
+        built = true;
+    }
+    err = cudaMemcpyToSymbol(g_pow, host_tab, sizeof(host_tab));
+    if (err == cudaSuccess && dev >= 0 && dev < 64) done[dev] = true;
+    return err;
+}
+
+}  // namespace bcn_b200

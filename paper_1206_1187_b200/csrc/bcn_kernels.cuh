@@ -1,0 +1,128 @@
+// bcn_kernels.cuh — launch-argument structs and launchers shared by the
+// kernels (bcn_kernels.cu) and the C-ABI host layer (bcn_capi.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "bcn_math.cuh"
+
+namespace bcn_b200 {
+
+enum Format : int { kFmtU64 = 0, kFmtF64 = 1, kFmtF32 = 2 };
+enum Engine : int { kEngAuto = 0, kEngBarrett = 1, kEngMontgomery = 2, kEngFP64 = 3, kEngStaged = 4 };
+
+inline int format_itemsize(int fmt) { return fmt == kFmtF32 ? 4 : 8; }
+
+// Contiguous fast path: `rows` full rows of 32 lanes x 32 bytes starting at the
+// 32-byte aligned `out`; element j of `out` has 2-exponent (e0 + 53 j) mod P.
+struct ContigArgs {
+    void* out;
+    uint64_t rows;
+    uint64_t e0;
+    Mult jump_row;  // 2^(53 * elements_per_row) mod m
+};
+
+// Interleaved region fast path (reference Layout::Interleaved,
+// parallel.cpp:24-33): physical slots q in [0, rows*ROW) of a region whose
+// slot q0 + q sits at worker w = (q0 + q) % width, element
+// i = i_base + (q0 + q) / width; logical index j = w * wpw + i.
+struct InterleavedArgs {
+    void* out;       // 32-byte aligned, physical slot q0 of the region
+    uint64_t rows;
+    uint64_t q0;     // region-relative slot of out[0]
+    uint64_t width;  // workers per physical row in this region (W or W-1)
+    uint64_t i_base;
+    uint64_t wpw;
+    uint64_t e0;     // exponent of logical element 0
+    uint64_t adv_b;  // ROW mod width
+    Mult jump_same;  // advance when w + adv_b < width
+    Mult jump_wrap;  // advance when the lane crosses a physical row
+};
+
+// Generic per-slot path with the reference's exact semantics, including the
+// u64 wrap of base_offset + start_w (parallel.cpp:63-64). One seed per slot.
+struct SlotArgs {
+    void* out;          // physical slot `slot0`
+    uint64_t slot0;
+    uint64_t count;
+    uint64_t n;         // plan.n
+    uint64_t wpw;       // plan.work_per_worker
+    uint32_t workers;   // plan.workers (effective)
+    int layout;         // 0 contiguous, 1 interleaved
+    uint64_t a_exp;     // (a - 3^33 - 1) mod P
+    uint64_t base_offset;
+};
+
+// Paper-style staged path: each thread runs L consecutive T=1 steps
+// (modified Barrett), the CTA tile is assembled in shared memory in logical
+// order and written with one TMA bulk store per tile.
+struct StagedArgs {
+    void* out;       // 16-byte aligned
+    uint64_t tiles;  // full tiles
+    uint64_t e0;
+    Mult jump_next;  // 2^(53 (gridDim.x * TILE - L)) mod m
+};
+
+struct SeedArgs {
+    const uint64_t* a;  // seed indices
+    const uint64_t* k;  // skip-ahead offsets
+    uint64_t* out;      // count * (steps ? steps : 1)
+    uint64_t count;
+    uint32_t steps;     // 0: state_at only; >0: emit next() `steps` times
+    int* error;         // set to 1 when any a is out of range
+};
+
+struct DigestArgs {
+    const void* buf;
+    uint64_t n;
+    uint32_t itemsize;
+    uint64_t index_base;
+    unsigned long long* out;  // [3] device accumulators
+};
+
+struct ConstArgs {
+    void* out;
+    uint64_t rows;  // rows of 32 lanes x 32 bytes
+    uint64_t value; // bit pattern replicated (8 bytes)
+};
+
+struct TransposeArgs {
+    const void* in;   // physical buffer
+    void* out;        // logical buffer
+    uint64_t p0;      // first physical slot of the region
+    uint64_t rows;    // region rows (elements per worker in the region)
+    uint64_t width;   // workers per row in the region
+    uint64_t wpw;
+    uint64_t i_base;  // element offset of the region inside each worker
+    uint32_t itemsize;
+};
+
+// Launchers (bcn_kernels.cu). Each returns the launch error, if any.
+cudaError_t launch_contig(int fmt, int engine, const ContigArgs& a, int grid, int block,
+                          cudaStream_t s);
+cudaError_t launch_interleaved(int fmt, int engine, const InterleavedArgs& a, int grid, int block,
+                               cudaStream_t s);
+cudaError_t launch_slots(int fmt, const SlotArgs& a, cudaStream_t s);
+cudaError_t launch_staged(int fmt, const StagedArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_seed(const SeedArgs& a, cudaStream_t s);
+cudaError_t launch_digest(const DigestArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_constant(const ConstArgs& a, int grid, int block, cudaStream_t s);
+cudaError_t launch_transpose(const TransposeArgs& a, cudaStream_t s);
+
+// Kernels launched through this library so far (process-wide).
+uint64_t launch_count();
+
+// Uploads the windowed power table to the current device (idempotent per device).
+cudaError_t upload_tables();
+
+// Resident CTAs per SM for the contiguous kernel of (fmt, engine) at `block`.
+int contig_blocks_per_sm(int fmt, int engine, int block);
+int interleaved_blocks_per_sm(int fmt, int engine, int block);
+
+constexpr int kStagedL = 15;          // odd: conflict-free strided smem stores
+constexpr int kStagedThreads = 256;
+constexpr int kContigThreads = 256;
+
+}  // namespace bcn_b200

@@ -1,0 +1,82 @@
+"""Device-side entry points beyond the reference API (all via the C ABI).
+
+* :func:`seed_states` — batched skip-ahead seeding kernel.
+* :func:`digest` — order-sensitive checksums of a device buffer.
+* :func:`fill_constant` — the Constant writer, the write-roofline denominator.
+* :func:`fill_multi` — one-process multi-GPU fill over contiguous shards.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+from .errors import InvalidArgument
+from .generator import kMinSeedIndex
+from .parallel import Engine, Format
+
+
+def _cuda(t: torch.Tensor, what: str) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or not t.is_contiguous():
+        raise InvalidArgument(f"{what}: expects a contiguous CUDA tensor")
+    return t
+
+
+def _stream(t: torch.Tensor, stream=None) -> ctypes.c_void_p:
+    s = stream if stream is not None else torch.cuda.current_stream(t.device)
+    return ctypes.c_void_p(int(getattr(s, "cuda_stream", s)))
+
+
+def seed_states(a: torch.Tensor, k: torch.Tensor, steps: int = 0, stream=None) -> torch.Tensor:
+    """state_at(a[t], k[t]) for every t (steps = 0), or the `steps` next()
+    residues after it (shape [count, steps]). a, k: int64/uint64 CUDA tensors
+    holding u64 values. Synchronous (reports out-of-range seeds)."""
+    _cuda(a, "seed_states")
+    _cuda(k, "seed_states")
+    if a.numel() != k.numel() or a.element_size() != 8 or k.element_size() != 8:
+        raise InvalidArgument("seed_states: a and k must be equal-length 64-bit tensors")
+    count = a.numel()
+    shape = (count,) if steps == 0 else (count, steps)
+    out = torch.empty(shape, dtype=torch.int64, device=a.device)
+    _lib.call("bcn_seed_states", ctypes.c_void_p(a.data_ptr()), ctypes.c_void_p(k.data_ptr()),
+              ctypes.c_void_p(out.data_ptr()), count, steps, a.device.index, _stream(a, stream))
+    return out
+
+
+def digest(buf: torch.Tensor, index_base: int = 0, stream=None) -> tuple[int, int, int]:
+    """(sum x, sum (index_base+i+1) x, xor x (2(index_base+i)+1)) mod 2^64 over
+    the raw 4- or 8-byte items of a CUDA tensor."""
+    _cuda(buf, "digest")
+    d = (ctypes.c_uint64 * 3)()
+    _lib.call("bcn_digest", ctypes.c_void_p(buf.data_ptr()), buf.numel(), buf.element_size(),
+              index_base, d, buf.device.index, _stream(buf, stream))
+    return d[0], d[1], d[2]
+
+
+def fill_constant(buf: torch.Tensor, pattern: int = 0x3FE0000000000000, stream=None) -> None:
+    """Write a fixed 8-byte pattern (default 0.5) with the fill's access pattern.
+    Asynchronous on the current torch stream."""
+    _cuda(buf, "fill_constant")
+    _lib.call("bcn_fill_constant", ctypes.c_void_p(buf.data_ptr()), buf.numel() * buf.element_size(),
+              pattern, buf.device.index, _stream(buf, stream))
+
+
+def fill_multi(outs: list[torch.Tensor], n: int, seed_index: int = kMinSeedIndex,
+               base_offset: int = 0, fmt: Format = Format.F64,
+               engine: Engine = Engine.Auto) -> None:
+    """Contiguous shards of make_plan(n, len(outs)) on each tensor's device; the
+    concatenation equals a single fill of n items. Synchronous."""
+    ndev = len(outs)
+    ptrs = (ctypes.c_void_p * ndev)(*[_cuda(t, "fill_multi").data_ptr() for t in outs])
+    devs = (ctypes.c_int * ndev)(*[t.device.index for t in outs])
+    _lib.call("bcn_fill_multi", ptrs, devs, ndev, n, int(fmt), seed_index,
+              base_offset & 0xFFFFFFFFFFFFFFFF, int(engine))
+
+
+def auto_engine(fmt: Format = Format.F64) -> Engine:
+    return Engine(_lib.lib().bcn_auto_engine(int(fmt)))
+
+
+def device_count() -> int:
+    return _lib.lib().bcn_device_count()

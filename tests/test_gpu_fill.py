@@ -1,0 +1,285 @@
+"""GPU parity tests: the sm_100a fill path vs the CPU oracle and the compiled
+reference, bit-exact. Mirrors the reference's own tests
+(tests/test_parallel.cpp, test_generator.cpp, test_cli.cpp) on the device path.
+"""
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+A0 = O.MIN_SEED
+ENGINES = ["Barrett", "Montgomery", "FP64", "Staged"]
+FORMATS = [(O.FMT_U64, torch.int64, np.uint64), (O.FMT_F64, torch.float64, np.float64),
+           (O.FMT_F32, torch.float32, np.float32)]
+
+
+def dev_fill(bcn, n, fmt=O.FMT_F64, *, workers=1, layout=0, seed=A0, base=0, engine="Auto",
+             offset=0, cuda="cuda:0"):
+    """Fill on the device through the public API; returns host numpy bytes."""
+    par = bcn.par
+    tdt = {O.FMT_U64: torch.int64, O.FMT_F64: torch.float64, O.FMT_F32: torch.float32}[fmt]
+    buf = torch.empty(n + offset, dtype=tdt, device=cuda)
+    plan = par.make_plan(n, workers, par.Layout(layout))
+    view = buf[offset:]
+    par.fill_format(view, plan, seed, bcn.Method.BarrettModified, base, par.Format(fmt),
+                    engine=par.Engine[engine], sync=True)
+    arr = view.cpu().numpy()
+    return arr.view(np.uint64) if fmt == O.FMT_U64 else arr
+
+
+def oracle_fill(oracle, n, fmt=O.FMT_F64, **kw):
+    out = oracle.fill(n, fmt, **kw)
+    return out
+
+
+def bits(a):
+    return np.ascontiguousarray(a).view(np.uint64 if a.itemsize == 8 else np.uint32)
+
+
+# --------------------------------------------------------------- config 1
+def test_config1_goldens_f64_u64(bcn, cuda, oracle):
+    """test_cli.cpp:76-86 and SURVEY Appendix A: n = 10^6 from a0, offset 0."""
+    u = dev_fill(bcn, 10**6, O.FMT_F64)
+    z = dev_fill(bcn, 10**6, O.FMT_U64)
+    assert hashlib.sha256(u.tobytes()).hexdigest() == \
+        "eb8dc6c55cbbf8dd7d64a7a08583401aecfcc89d22fa112aa6d83e12a3d8fa0f"
+    assert hashlib.sha256(z.tobytes()).hexdigest() == \
+        "05ad1e442fe2fe60371779e0b73add6454f16304f0375dd9f0a0b82bce2db223"
+    assert int(z[0]) == 2138759898642167
+    assert int(z[-1]) == 2099187967082161
+    assert int(z.sum(dtype=np.uint64)) == 11204447702781092184
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("fmt", [O.FMT_U64, O.FMT_F64, O.FMT_F32])
+def test_engines_formats_bit_exact(bcn, cuda, oracle, engine, fmt):
+    """Every reduction engine and output format equals the oracle bit for bit
+    (the reference's method-identity property, test_generator.cpp:70-83)."""
+    n = 3 * 2**18 + 77  # ragged: head/tail paths around the vector body
+    got = dev_fill(bcn, n, fmt, engine=engine, base=12345)
+    want = oracle.fill(n, fmt, base_offset=12345)
+    assert np.array_equal(bits(got), bits(want))
+
+
+@pytest.mark.parametrize("offset", [1, 2, 3, 5])
+def test_misaligned_outputs(bcn, cuda, oracle, offset):
+    for fmt in (O.FMT_F64, O.FMT_F32):
+        got = dev_fill(bcn, 5000, fmt, offset=offset)
+        assert np.array_equal(bits(got), bits(oracle.fill(5000, fmt)))
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 31, 127, 128, 129, 1023, 4096, 100003])
+def test_small_and_ragged_sizes(bcn, cuda, oracle, n):
+    for engine in ("Barrett", "FP64"):
+        got = dev_fill(bcn, n, O.FMT_U64, engine=engine)
+        assert np.array_equal(got, oracle.fill(n, O.FMT_U64))
+
+
+# ------------------------------------------------------- plan invariance
+@pytest.mark.parametrize("workers", [1, 2, 3, 4, 8, 16, 7, 1000, 99999])
+def test_worker_and_layout_invariance(bcn, cuda, oracle, reference, workers):
+    """test_parallel.cpp:82-96 / :98-105: logical output is W-invariant; the
+    physical Interleaved buffer equals the reference's and deinterleaves to
+    the serial stream."""
+    n = 100000
+    serial = oracle.fill(n, O.FMT_F64)
+    for layout in (0, 1):
+        got = dev_fill(bcn, n, O.FMT_F64, workers=workers, layout=layout)
+        want = reference.fill(n, O.FMT_F64, workers=min(workers, 64), layout=layout) \
+            if workers <= 64 else oracle.fill(n, O.FMT_F64, workers=workers, layout=layout)
+        assert np.array_equal(bits(got), bits(want))
+        if layout == 1:
+            plan = bcn.par.make_plan(n, workers, bcn.Layout.Interleaved)
+            logical = bcn.par.deinterleave(torch.from_numpy(got).to(cuda), plan).cpu().numpy()
+            assert np.array_equal(bits(logical), bits(serial))
+        else:
+            assert np.array_equal(bits(got), bits(serial))
+
+
+def test_interleaved_ragged_million(bcn, cuda, reference):
+    """test_parallel.cpp:98-105: W = 7, n = 10^6, Interleaved."""
+    got = dev_fill(bcn, 10**6, O.FMT_F64, workers=7, layout=1)
+    assert np.array_equal(bits(got), bits(reference.fill(10**6, O.FMT_F64, workers=7, layout=1)))
+
+
+@pytest.mark.parametrize("engine", ["Barrett", "Montgomery", "FP64"])
+@pytest.mark.parametrize("fmt", [O.FMT_U64, O.FMT_F32])
+def test_interleaved_engines_formats(bcn, cuda, oracle, engine, fmt):
+    n = 200003
+    for w in (3, 33, 130):
+        got = dev_fill(bcn, n, fmt, workers=w, layout=1, engine=engine, base=999)
+        want = oracle.fill(n, fmt, workers=w, layout=1, base_offset=999)
+        assert np.array_equal(bits(got), bits(want))
+
+
+# ----------------------------------------------------- offsets and wraps
+def test_base_offset_windows(bcn, cuda, oracle):
+    """test_parallel.cpp:131-138 and test_cli.cpp:116-125 (chunked == single)."""
+    whole = dev_fill(bcn, 1 << 20, O.FMT_U64)
+    chunks = [dev_fill(bcn, 1 << 18, O.FMT_U64, base=c << 18, workers=3) for c in range(4)]
+    assert np.array_equal(np.concatenate(chunks), whole)
+
+
+def test_period_wrap_golden(bcn, cuda):
+    """fill_residues(n=6, a0, base_offset=P-3) re-emits z0 at k=P."""
+    got = dev_fill(bcn, 6, O.FMT_U64, base=O.PERIOD - 3)
+    assert [int(x) for x in got] == [1867496909077246, 5488691822377859, 4258649398211344,
+                                     2138759898642167, 906908310809773, 121054228244396]
+
+
+def test_period_wrap_large_window(bcn, cuda, oracle):
+    for fmt in (O.FMT_U64, O.FMT_F64):
+        got = dev_fill(bcn, 300000, fmt, base=O.PERIOD - 150000, engine="FP64")
+        assert np.array_equal(bits(got), bits(oracle.fill(300000, fmt, base_offset=O.PERIOD - 150000)))
+
+
+def test_far_offset_interleaved_golden(bcn, cuda):
+    """a = 2^53, base_offset = 2^40, W = 3, Interleaved."""
+    got = dev_fill(bcn, 6, O.FMT_U64, seed=1 << 53, base=1 << 40, workers=3, layout=1)
+    assert [int(x) for x in got] == [1584414649962571, 4289752975226581, 752696664753940,
+                                     663488620216616, 2266604546227133, 4919938457993333]
+
+
+@pytest.mark.parametrize("layout", [0, 1])
+def test_u64_wrap_of_base_offset_matches_reference(bcn, cuda, reference, layout):
+    """base_offset + start_w wraps mod 2^64 in the reference (parallel.cpp:63-64);
+    the device path reproduces that exactly for W > 1."""
+    n, w = 50000, 5
+    base = (1 << 64) - 23456
+    got = dev_fill(bcn, n, O.FMT_U64, workers=w, layout=layout, base=base)
+    want = reference.fill(n, O.FMT_U64, workers=w, layout=layout, base_offset=base)
+    assert np.array_equal(got, want)
+
+
+def test_seed_extremes(bcn, cuda, oracle):
+    for seed in (A0, A0 + 1, (1 << 53) - 1, 1 << 53):
+        got = dev_fill(bcn, 70001, O.FMT_U64, seed=seed, base=seed % 1000003)
+        assert np.array_equal(got, oracle.fill(70001, O.FMT_U64, seed_index=seed,
+                                                  base_offset=seed % 1000003))
+
+
+# ------------------------------------------------------------- host buffers
+def test_host_numpy_output_chunked(bcn, cuda, oracle):
+    """Host (pageable) span like the reference's std::span fill: > one 64 MiB chunk."""
+    n = (1 << 24) + 12345
+    out = np.empty(n, dtype=np.float64)
+    plan = bcn.par.make_plan(n, 3)
+    bcn.par.fill(out, plan, A0, base_offset=77)
+    assert oracle.digest(bits(out)) == oracle.digest(bits(oracle.fill(n, O.FMT_F64, base_offset=77,
+                                                                      workers=3)))
+
+
+def test_host_pinned_output(bcn, cuda, oracle):
+    n = (1 << 23) + 3
+    out = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    bcn.par.fill_float(out, bcn.par.make_plan(n, 1), A0)
+    assert np.array_equal(bits(out.numpy()), bits(oracle.fill(n, O.FMT_F32)))
+
+
+# --------------------------------------------------------------- errors
+def test_errors_before_work(bcn, cuda):
+    """Size and seed checks happen before any device work (parallel.cpp:59-61,
+    generator.cpp:33-35); W > 1 with a bad seed raises instead of aborting."""
+    buf = torch.full((100,), -1.0, dtype=torch.float64, device=cuda)
+    with pytest.raises(bcn.InvalidArgument):
+        bcn.par.fill(buf[:99], bcn.par.make_plan(100, 2), A0)
+    with pytest.raises(bcn.OutOfRange):
+        bcn.par.fill(buf, bcn.par.make_plan(100, 4), A0 - 1)
+    with pytest.raises(bcn.OutOfRange):
+        bcn.par.fill(buf, bcn.par.make_plan(100, 4), (1 << 53) + 1)
+    with pytest.raises(bcn.InvalidArgument):
+        bcn.par.fill_residues(buf, bcn.par.make_plan(100, 1), A0)  # dtype mismatch
+    torch.cuda.synchronize()
+    assert bool((buf == -1.0).all())
+    with pytest.raises(bcn.InvalidArgument):
+        bcn.par.deinterleave(buf, bcn.par.make_plan(100, 2))  # not Interleaved
+
+
+# ------------------------------------------------------------ seeding (C4)
+def test_seed_states_stress(bcn, cuda, oracle):
+    """2^20 streams with arbitrary (a, k) incl. the period wrap,
+    a = 2^53 and k near 2^64; each compared with state_at (+ next walks)."""
+    rng = np.random.Generator(np.random.MT19937(0x12061187))
+    count = 1 << 20
+    a = rng.integers(A0, (1 << 53) + 1, size=count, dtype=np.uint64)
+    k = rng.integers(0, np.iinfo(np.uint64).max, size=count, dtype=np.uint64, endpoint=True)
+    forced_k = [O.PERIOD - 2, O.PERIOD - 1, O.PERIOD, O.PERIOD + 1, 0, (1 << 64) - 1, 2 * O.PERIOD]
+    k[:len(forced_k)] = forced_k
+    a[len(forced_k):len(forced_k) + 3] = [1 << 53, A0, (1 << 53) - 1]
+    ta = torch.from_numpy(a.view(np.int64)).to(cuda)
+    tk = torch.from_numpy(k.view(np.int64)).to(cuda)
+    got = bcn.device.seed_states(ta, tk).cpu().numpy().view(np.uint64)
+    assert np.array_equal(got, oracle.seed_batch(a, k))
+    sub = 1 << 14
+    walks = bcn.device.seed_states(ta[:sub], tk[:sub], steps=64).cpu().numpy().view(np.uint64)
+    assert np.array_equal(walks, oracle.seed_batch(a[:sub], k[:sub], steps=64))
+    bad = ta[:4].clone()
+    bad[2] = A0 - 1
+    with pytest.raises(bcn.OutOfRange):
+        bcn.device.seed_states(bad, tk[:4])
+
+
+# ------------------------------------------------------------- utilities
+def test_digest_and_constant(bcn, cuda, oracle):
+    got = dev_fill(bcn, 1 << 20, O.FMT_U64)
+    t = torch.from_numpy(got.view(np.int64)).to(cuda)
+    assert bcn.device.digest(t, index_base=5) == oracle.digest(got, index_base=5)
+    c = torch.empty(1 << 20, dtype=torch.float64, device=cuda)
+    bcn.device.fill_constant(c)
+    torch.cuda.synchronize()
+    assert bool((c == 0.5).all())
+
+
+def test_fill_multi_concatenation(bcn, cuda, oracle):
+    """make_plan(n, G) contiguous shards (one per 'device'; two shards on GPU 0
+    here) concatenate to the single fill."""
+    n = 1_000_003
+    eff, wpw = oracle.make_plan(n, 2)
+    outs = [torch.empty(wpw, dtype=torch.float64, device=cuda),
+            torch.empty(n - wpw, dtype=torch.float64, device=cuda)]
+    bcn.device.fill_multi(outs, n, base_offset=31)
+    got = torch.cat(outs).cpu().numpy()
+    assert np.array_equal(bits(got), bits(oracle.fill(n, O.FMT_F64, base_offset=31, workers=2)))
+
+
+def test_scalar_generator_api(bcn, cuda, oracle):
+    g = bcn.gen
+    s = g.seed_from_index(A0)
+    assert s.z == 4258649398211344
+    assert g.next(s) == 2138759898642167 and s.k == 1
+    assert g.state_at(A0, 1000).z == 5492007519572011
+    assert g.seed_from_index(1 << 53).z == 1895384862748766
+
+
+# ------------------------------------------------------- full-size (C2)
+@pytest.mark.slow
+def test_config2_full_size_digests(bcn, cuda, oracle):
+    """C2: 2^30 doubles on one B200 vs the oracle, per-2^24-chunk digests, plus a
+    size-independent check: chunked (base_offset) fills equal the single fill."""
+    n = 1 << 30
+    buf = torch.empty(n, dtype=torch.float64, device=cuda)
+    bcn.par.fill(buf, bcn.par.make_plan(n, 1), A0, sync=True)
+    chunk = 1 << 24
+    host = np.empty(chunk, dtype=np.float64)
+    for c in range(0, n // chunk, 9):  # every 9th chunk (8 chunks incl. first/last region)
+        oracle.fill(chunk, O.FMT_F64, base_offset=c * chunk, out=host)
+        dd = bcn.device.digest(buf[c * chunk:(c + 1) * chunk].view(torch.int64))
+        assert dd == oracle.digest(bits(host)), f"chunk {c}"
+    last = buf[-chunk:].view(torch.int64)
+    oracle.fill(chunk, O.FMT_F64, base_offset=n - chunk, out=host)
+    assert bcn.device.digest(last) == oracle.digest(bits(host))
+    whole = bcn.device.digest(buf.view(torch.int64))
+    parts = [0, 0]
+    half = torch.empty(n // 2, dtype=torch.float64, device=cuda)
+    for h in range(2):
+        bcn.par.fill(half, bcn.par.make_plan(n // 2, 1), A0, base_offset=h * (n // 2), sync=True)
+        d = bcn.device.digest(half.view(torch.int64), index_base=h * (n // 2))
+        parts = [(parts[0] + d[0]) % (1 << 64), (parts[1] + d[1]) % (1 << 64)]
+    assert parts == [whole[0], whole[1]]
