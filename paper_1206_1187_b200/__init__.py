@@ -10,6 +10,7 @@ residues, doubles or floats, computed by sm_100a kernels behind the C ABI in
 * :mod:`.device`    — device-only extras (seeding kernel, digests, Constant writer,
   multi-GPU fill)
 """
+from . import device
 from . import generator as gen
 from . import parallel as par
 from .errors import CudaError, DomainError, InvalidArgument, OutOfRange
@@ -18,7 +19,7 @@ from .generator import (GeneratorState, Method, kInvModulus, kMaxSeedIndex, kMin
 from .parallel import Engine, Format, Layout, PartitionPlan
 
 __all__ = [
-    "gen", "par", "CudaError", "DomainError", "InvalidArgument", "OutOfRange",
+    "gen", "par", "device", "CudaError", "DomainError", "InvalidArgument", "OutOfRange",
     "GeneratorState", "Method", "Layout", "Format", "Engine", "PartitionPlan",
     "kModulus", "kMinSeedIndex", "kMaxSeedIndex", "kPeriod", "kInvModulus",
 ]
