@@ -54,6 +54,9 @@ def parse() -> argparse.Namespace:
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--sweep", default="", help="write a format x engine x size sweep (JSON lines)")
+    p.add_argument("--ab", default="", help="interleaved engine A/B for --fmt, JSON lines to FILE")
+    p.add_argument("--workload", default="c2", choices=["c2", "c5"],
+                   help="c2: 2^log2n per GPU (weak scaling); c5: 2^36 total index-sharded (strong)")
     return p.parse_args()
 
 
@@ -172,6 +175,37 @@ def run_reference(args) -> None:
 
 
 # ------------------------------------------------------------------ ours
+ENGINE_NAMES = {"auto": "Auto", "barrett": "Barrett", "montgomery": "Montgomery", "fp64": "FP64",
+                "staged": "Staged", "bulk": "Bulk"}
+
+
+def kernel_name(fmt: int, engine: int) -> str:
+    """Template instance name of the dominant kernel for (format, engine)."""
+    if engine == 4:
+        return f"void k_fill_staged<{fmt}>(StagedArgs)"
+    if engine == 5:
+        return f"void k_fill_bulk<{fmt}, 3>(ContigArgs)"
+    return f"void k_fill_contig<{fmt}, {engine}>(ContigArgs)"
+
+
+def ncu_traffic(kernel: str) -> tuple[float | None, str | None]:
+    """dram read+write bytes per launch of `kernel` from the newest committed
+    `ncu --set full` summary under profiles/ (tools/ncu_summary.py)."""
+    import glob
+
+    best = None
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_full_*.json"))):
+        try:
+            with open(path) as f:
+                rows = json.load(f)
+        except (OSError, ValueError):
+            continue
+        for r in rows if isinstance(rows, list) else []:
+            if r.get("kernel", "").strip() == kernel and "traffic_bytes" in r:
+                best = (r["traffic_bytes"], os.path.relpath(path, ROOT))
+    return best if best else (None, None)
+
+
 def main() -> None:
     args = parse()
     if args.impl == "reference":
@@ -182,7 +216,7 @@ def main() -> None:
     import torch.distributed as dist
 
     import paper_1206_1187_b200 as B
-    from paper_1206_1187_b200 import _lib
+    from paper_1206_1187_b200 import _lib, sharding
     from paper_1206_1187_b200 import build as bld
 
     bld.build()
@@ -198,28 +232,39 @@ def main() -> None:
         if world > 1:
             dist.barrier()
 
-    def max_over_ranks(x: float) -> float:
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
     fmt = B.Format[args.fmt.upper()]
-    engine = B.Engine.Auto if args.engine == "auto" else B.Engine[
-        {"barrett": "Barrett", "montgomery": "Montgomery", "fp64": "FP64", "staged": "Staged"}[args.engine]]
+    engine = B.Engine[ENGINE_NAMES[args.engine]]
     resolved = B.Engine(_lib.lib().bcn_auto_engine(int(fmt))) if engine == B.Engine.Auto else engine
     isz = FMT_ITEMSIZE[args.fmt]
-    n = 1 << args.log2n
     tdtype = {"f64": torch.float64, "u64": torch.int64, "f32": torch.float32}[args.fmt]
-    buf = torch.empty(n, dtype=tdtype, device=dev)
-    plan = B.par.make_plan(n, 1)
-    base = rank * n
     stream = torch.cuda.current_stream(dev)
+    lib = _lib.lib()
 
-    def fill_once(out=buf, b=base):
-        B.par.fill_format(out, plan, A0, B.Method.BarrettModified, b, fmt, engine=engine,
-                          stream=stream)
+    # Work of this rank: a list of (base_offset, count) launches per step.
+    if args.workload == "c2":
+        n_rank = 1 << args.log2n
+        start, count = sharding.shard(world * n_rank, world, rank)
+        pieces = [(start, count)]
+        total_items = world * n_rank
+        workload = (f"C2: fill 2^{args.log2n} {args.fmt} variates per GPU from seed index a0 = "
+                    f"3^33+100; rank r at base_offset r*2^{args.log2n} (weak scaling)")
+        scaling = "weak"
+    else:
+        total_items = 1 << 36
+        start, count = sharding.shard(total_items, world, rank)
+        pieces = list(sharding.chunks(start, count, 1 << 32))
+        workload = (f"C5: 2^36 {args.fmt} variates from a0 index-sharded over {world} GPU(s), "
+                    "launches of <= 2^32 items into one resident buffer (strong scaling)")
+        scaling = "strong"
+    buf_items = max(c for _, c in pieces)
+    buf = torch.empty(buf_items, dtype=tdtype, device=dev)
+    plans = {c: B.par.make_plan(c, 1) for _, c in pieces}
+    raw = buf.view(torch.int64) if isz == 8 else buf.view(torch.int32)
+
+    def step():
+        for b, c in pieces:
+            B.par.fill_format(buf[:c], plans[c], A0, B.Method.BarrettModified, b, fmt,
+                              engine=engine, stream=stream)
 
     def timed(fn, steps, warmup):
         """Per-call CUDA-event durations (ms), total ms and the number of our
@@ -229,31 +274,31 @@ def main() -> None:
         barrier()
         torch.cuda.synchronize(dev)
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
-        lc0 = _lib.lib().bcn_launch_count()
+        lc0 = lib.bcn_launch_count()
         evs[0].record(stream)
         for i in range(steps):
             fn()
             evs[i + 1].record(stream)
         torch.cuda.synchronize(dev)
-        launched = _lib.lib().bcn_launch_count() - lc0
+        launched = lib.bcn_launch_count() - lc0
         per = [evs[i].elapsed_time(evs[i + 1]) for i in range(steps)]
         total = evs[0].elapsed_time(evs[-1])
         barrier()
         return per, total, launched
 
     # Constant writer (the paper's memory ceiling) with the identical pattern.
-    cbuf = buf.view(torch.int64) if isz == 8 else buf.view(torch.int32)
-    const_per, _, _ = timed(lambda: B.device.fill_constant(cbuf, stream=stream),
-                                   max(20, args.steps // 4), 5)
-    const_gbs = n * isz / (statistics.mean(const_per) * 1e-3) / 1e9
+    const_per, _, _ = timed(lambda: B.device.fill_constant(raw, stream=stream),
+                            max(20, args.steps // 4), 5)
+    const_gbs = buf_items * isz / (statistics.mean(const_per) * 1e-3) / 1e9
 
-    # Headline: device-resident fill.
+    # Headline: device-resident fill, every step writes this rank's whole share.
     with ClockSampler(local) as clocks:
-        per, total_ms, launches = timed(fill_once, args.steps, args.warmup)
-    total_ms = max_over_ranks(total_ms)
-    value = world * n * args.steps / (total_ms * 1e-3)
-    avg_launch_ms = statistics.mean(per)
-    achieved_gbs = n * isz / (avg_launch_ms * 1e-3) / 1e9
+        per, total_ms, launches = timed(step, args.steps, args.warmup)
+    total_ms = sharding.max_over_ranks(total_ms, dev)
+    value = total_items * args.steps / (total_ms * 1e-3)
+    avg_step_ms = statistics.mean(per)
+    launches_per_step = max(1, launches // args.steps)
+    achieved_gbs = count * isz / (avg_step_ms * 1e-3) / 1e9  # this rank's kernel bytes / time
 
     peaks = {}
     try:
@@ -262,29 +307,44 @@ def main() -> None:
     except OSError:
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    peak_src = "MEASURED_PEAKS.json hbm_gbs (copy)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"
+    peak_src = "MEASURED_PEAKS.json hbm_gbs (STREAM copy, measured)" if "hbm_gbs" in peaks \
+        else "fallback 6.65 TB/s (B200_PROFILING.md)"
 
-    # Parity spot check of this very buffer (size-independent, no oracle):
-    # the digest of the timed output equals the digest of a chunked refill.
-    d_full = B.device.digest(buf.view(torch.int64) if isz == 8 else buf.view(torch.int32),
-                             index_base=base)
+    # Verification (untimed): digest of every launch's output, combined over
+    # the shards with a 24-byte all-gather (the only collective).
+    parts = []
+    for b, c in pieces:
+        B.par.fill_format(buf[:c], plans[c], A0, B.Method.BarrettModified, b, fmt, engine=engine,
+                          stream=stream)
+        parts.append(B.device.digest(raw[:c], index_base=b))
+    local_digest = sharding.combine(parts)
+    global_digest = sharding.allgather_digest(local_digest, dev) if world > 1 else local_digest
+    verified = None
+    if args.workload == "c5" and args.fmt == "f64":
+        try:
+            with open(os.path.join(ROOT, "tests", "golden", "c5_digest.json")) as f:
+                want = [int(x) for x in json.load(f)["digest"]]
+            verified = list(global_digest) == want
+        except (OSError, ValueError, KeyError):
+            verified = None
 
-    # End to end through the public API with a pinned host output.
+    # End to end through the public API: pinned HOST output, D2H inside.
     e2e = None
-    if not args.no_e2e:
-        host = torch.empty(n, dtype=tdtype, pin_memory=True)
-        hplan = B.par.make_plan(n, 1)
-        B.par.fill_format(host, hplan, A0, B.Method.BarrettModified, base, fmt, engine=engine)
+    if not args.no_e2e and args.workload == "c2":
+        host = torch.empty(count, dtype=tdtype, pin_memory=True)
+        hplan = B.par.make_plan(count, 1)
+        B.par.fill_format(host, hplan, A0, B.Method.BarrettModified, start, fmt, engine=engine)
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            B.par.fill_format(host, hplan, A0, B.Method.BarrettModified, base, fmt, engine=engine)
-        dt = max_over_ranks(time.perf_counter() - t0)
+            B.par.fill_format(host, hplan, A0, B.Method.BarrettModified, start, fmt, engine=engine)
+        dt = sharding.max_over_ranks(time.perf_counter() - t0, dev)
         barrier()
-        e2e = {"value": world * n * args.e2e_steps / dt, "unit": UNIT, "h2d_bytes_per_step": 0,
-               "d2h_bytes_per_step": n * isz, "steps": args.e2e_steps,
-               "note": "inputs are scalar kernel arguments (seed index, offset, count): no H2D "
-                       "buffer; D2H = the filled array, pinned host memory"}
+        e2e = {"value": total_items * args.e2e_steps / dt, "unit": UNIT, "h2d_bytes_per_step": 0,
+               "d2h_bytes_per_step": count * isz, "steps": args.e2e_steps,
+               "note": "bcn_fill with a pinned host pointer: chunked device generation + D2H on "
+                       "two streams; inputs are scalar kernel arguments (seed index, offset, "
+                       "count), so there is no H2D buffer"}
         del host
 
     cpu = None
@@ -293,76 +353,106 @@ def main() -> None:
         n_cpu = 1 << 27
         rate, secs = reference_rate(n_cpu, threads)
         cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
-               "sample": f"reference par::fill (oracle/_ref) of 2^27 doubles with W={threads} "
-                         f"threads, {secs:.2f} s"}
+               "sample": f"reference par::fill (oracle/_ref = unmodified /root/reference sources, "
+                         f"g++ -O3) of 2^27 doubles, W={threads} threads, {secs:.2f} s"}
 
-    sweep_rows = []
-    if args.sweep:
-        sweep_rows = run_sweep(B, dev, stream, timed, buf)
+    ab_rows = run_ab(B, torch, dev, stream, timed, buf, fmt, args.ab) if args.ab else []
+    sweep_rows = run_sweep(B, dev, stream, timed) if args.sweep else []
 
     if rank == 0:
+        kname = kernel_name(int(fmt), int(resolved))
+        traffic, traffic_src = ncu_traffic(kname)
+        bytes_per_launch = count * isz / launches_per_step
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": args.fmt,
+            "scaling": scaling, "vs_baseline": None, "dtype": args.fmt,
             "data": "synthetic: the generator has no inputs; output is the alpha_{2,3} stream",
             "config": {
-                "workload": f"C2: fill 2^{args.log2n} {args.fmt} variates per GPU from seed index "
-                            "a0 = 3^33+100, rank r at base_offset r*2^" + str(args.log2n),
-                "n_per_gpu": n, "format": args.fmt, "engine": B.par.Engine(resolved).name,
-                "layout": "contiguous", "parallelism": f"index-sharded x{world}",
-                "l2": "output 8 GiB per step >> 126 MB L2 (no flush needed)",
+                "workload": workload, "items_per_step": total_items, "format": args.fmt,
+                "engine": B.par.Engine(resolved).name, "layout": "contiguous",
+                "parallelism": f"index-sharded x{world}, no data-path collective",
+                "l2": f"output {buf_items * isz / 2**30:.0f} GiB per launch >> 126 MB L2 "
+                      "(inputs larger than L2, no flush needed)",
             },
             "gbs_written": value * isz / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
-                         "frac": achieved_gbs / peak, "traffic": None, "peak_source": peak_src,
-                         "kernel": "k_fill_contig", "bytes_per_launch": n * isz,
-                         "avg_launch_ms": avg_launch_ms,
+                         "frac": achieved_gbs / peak,
+                         "traffic": traffic, "traffic_source": traffic_src,
+                         "peak_source": peak_src, "kernel": kname,
+                         "bytes_per_launch": bytes_per_launch,
+                         "algorithmic_bytes_per_variate": isz,
+                         "avg_launch_ms": avg_step_ms / launches_per_step,
                          "constant_writer_gbs": const_gbs,
                          "frac_of_constant_writer": achieved_gbs / const_gbs},
             "e2e": e2e,
             "cpu_baseline": cpu,
             "gpu_launches": int(launches),
             "clocks": clocks.summary(),
-            "digest": [str(x) for x in d_full],
+            "digest": [str(x) for x in global_digest],
+            "digest_verified_vs_oracle": verified,
         }
-        if sweep_rows:
-            with open(args.sweep, "w") as f:
-                for r in sweep_rows:
-                    f.write(json.dumps(r) + "\n")
-            line["sweep_file"] = args.sweep
+        for name, rows in (("ab_file", ab_rows), ("sweep_file", sweep_rows)):
+            if rows:
+                path = args.ab if name == "ab_file" else args.sweep
+                with open(path, "w") as f:
+                    for r in rows:
+                        f.write(json.dumps(r) + "\n")
+                line[name] = path
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
-def run_sweep(B, dev, stream, timed, big) -> list[dict]:
-    """formats x engines x sizes, device-resident, GB/s."""
+def run_ab(B, torch, dev, stream, timed, buf, fmt, path) -> list[dict]:
+    """Interleaved A/B of every engine for one format: 15 rounds x 6 launches
+    each, round-robin, so drift affects all engines alike."""
+    plan = B.par.make_plan(buf.numel(), 1)
+    engines = [e for e in B.Engine if e != B.Engine.Auto]
+    times = {e.name: [] for e in engines}
+    times["Constant"] = []
+    raw = buf.view(torch.int64) if buf.element_size() == 8 else buf.view(torch.int32)
+    for _ in range(15):
+        for e in engines:
+            per, _, _ = timed(lambda: B.par.fill_format(buf, plan, A0, B.Method.BarrettModified, 0,
+                                                        fmt, engine=e, stream=stream), 6, 1)
+            times[e.name] += per
+        per, _, _ = timed(lambda: B.device.fill_constant(raw, stream=stream), 6, 1)
+        times["Constant"] += per
+    nbytes = buf.numel() * buf.element_size()
+    rows = []
+    for k, v in times.items():
+        med = statistics.median(v)
+        rows.append({"fmt": B.Format(fmt).name, "engine": k, "median_ms": med, "min_ms": min(v),
+                     "gbs_median": nbytes / (med * 1e-3) / 1e9, "samples": len(v)})
+        print(json.dumps(rows[-1]), file=sys.stderr, flush=True)
+    return rows
+
+
+def run_sweep(B, dev, stream, timed) -> list[dict]:
+    """formats x engines x sizes 2^28..2^32, device-resident."""
     import torch
 
     rows = []
-    for log2n in (28, 30, 32):
+    for log2n in (28, 29, 30, 31, 32):
         for fmt in ("u64", "f64", "f32"):
             isz = FMT_ITEMSIZE[fmt]
             nbytes = (1 << log2n) * isz
-            if nbytes > 40 << 30:
-                continue
             tdt = {"f64": torch.float64, "u64": torch.int64, "f32": torch.float32}[fmt]
             out = torch.empty(1 << log2n, dtype=tdt, device=dev)
             plan = B.par.make_plan(1 << log2n, 1)
-            for eng in ("Barrett", "Montgomery", "FP64", "Staged"):
-                f = B.Format[fmt.upper()]
-                e = B.Engine[eng]
-                per, _, _ = timed(lambda: B.par.fill_format(out, plan, A0, B.Method.BarrettModified, 0,
-                                                         f, engine=e, stream=stream), 10, 3)
+            f = B.Format[fmt.upper()]
+            for e in [e for e in B.Engine if e != B.Engine.Auto]:
+                per, _, _ = timed(lambda: B.par.fill_format(out, plan, A0, B.Method.BarrettModified,
+                                                            0, f, engine=e, stream=stream), 10, 3)
                 ms = statistics.median(per)
-                rows.append({"log2n": log2n, "fmt": fmt, "engine": eng, "ms": ms,
+                rows.append({"log2n": log2n, "fmt": fmt, "engine": e.name, "ms": ms,
                              "gbs": nbytes / (ms * 1e-3) / 1e9,
                              "gvariates_s": (1 << log2n) / (ms * 1e-3) / 1e9})
                 print(json.dumps(rows[-1]), file=sys.stderr, flush=True)
-            cper, _, _ = timed(lambda: B.device.fill_constant(out.view(torch.int32) if isz == 4 else out.view(torch.int64),
-                                                           stream=stream), 10, 3)
-            ms = statistics.median(cper)
+            raw = out.view(torch.int32) if isz == 4 else out.view(torch.int64)
+            per, _, _ = timed(lambda: B.device.fill_constant(raw, stream=stream), 10, 3)
+            ms = statistics.median(per)
             rows.append({"log2n": log2n, "fmt": fmt, "engine": "Constant", "ms": ms,
                          "gbs": nbytes / (ms * 1e-3) / 1e9})
             print(json.dumps(rows[-1]), file=sys.stderr, flush=True)

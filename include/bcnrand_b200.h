@@ -63,14 +63,15 @@ typedef enum bcn_engine {
     BCN_ENGINE_BARRETT = 1,    /* Shoup-form Barrett jump multiply         */
     BCN_ENGINE_MONTGOMERY = 2, /* Montgomery REDC jump multiply            */
     BCN_ENGINE_FP64 = 3,       /* exact FP64-pipe jump multiply            */
-    BCN_ENGINE_STAGED = 4      /* paper T=1 modified Barrett + TMA bulk store */
+    BCN_ENGINE_STAGED = 4,     /* paper T=1 modified Barrett + TMA bulk store */
+    BCN_ENGINE_BULK = 5        /* FP64 jump streams staged in smem + TMA bulk store */
 } bcn_engine;
 
 /* ---- library ---------------------------------------------------------- */
 int bcn_abi_version(void);
 /* Message for the calling thread's most recent non-OK status ("" if none). */
 const char* bcn_last_error(void);
-/* Name of an engine ("barrett", "montgomery", "fp64", "staged", "auto"). */
+/* Name of an engine ("auto", "barrett", "montgomery", "fp64", "staged", "bulk"). */
 const char* bcn_engine_name(int engine);
 /* Number of visible CUDA devices (0 when none; never an error). */
 int bcn_device_count(void);

@@ -118,7 +118,7 @@ bcn_status get_ctx(int device, DevCtx** out) {
 int resolve_engine(int engine, int fmt) {
     if (engine != kEngAuto) return engine;
     (void)fmt;
-    return kEngBarrett;  // measured best (profiles/)
+    return kEngFP64;  // measured best (profiles/)
 }
 
 int blocks_per_sm(DevCtx* c, int fmt, int engine, bool interleaved) {
@@ -212,9 +212,18 @@ cudaError_t enqueue_affine(const FillJob& j, char* dptr, uint64_t slot0, uint64_
         c.out = dptr + head * isz;
         c.rows = rows;
         c.e0 = exp_add(e_first, head);
-        c.jump_row = mult_for_steps(static_cast<__int128>(row));
-        const int grid = grid_for_rows(j.ctx, j.fmt, j.engine, false, rows);
-        e = launch_contig(j.fmt, j.engine, c, grid, kContigThreads, j.stream);
+        if (j.engine == kEngBulk) {
+            // Streams advance one 16-row tile per step (k_fill_bulk).
+            c.jump_row = mult_for_steps(static_cast<__int128>(row) * kBulkTileRows);
+            const uint64_t tiles = (rows + kBulkTileRows - 1) / kBulkTileRows;
+            const uint64_t persistent = static_cast<uint64_t>(j.ctx->sms) * bulk_blocks_per_sm(j.fmt);
+            const int grid = static_cast<int>(std::max<uint64_t>(1, std::min(persistent, tiles)));
+            e = launch_bulk(j.fmt, c, grid, j.stream);
+        } else {
+            c.jump_row = mult_for_steps(static_cast<__int128>(row));
+            const int grid = grid_for_rows(j.ctx, j.fmt, j.engine, false, rows);
+            e = launch_contig(j.fmt, j.engine, c, grid, kContigThreads, j.stream);
+        }
         if (e != cudaSuccess) return e;
     }
     const uint64_t done = head + rows * row;
@@ -232,7 +241,9 @@ cudaError_t enqueue_region(const FillJob& j, char* dptr, uint64_t slot0, uint64_
         return enqueue_affine(j, dptr, slot0, count, exp_add(e_elem0, i_base + q_begin));
     }
     const int isz = format_itemsize(j.fmt);
-    const int engine = j.engine == kEngStaged ? kEngBarrett : j.engine;
+    // The staged paths are contiguous-only; interleaved regions use the
+    // matching direct-store engine.
+    const int engine = j.engine == kEngStaged ? kEngBarrett : j.engine == kEngBulk ? kEngFP64 : j.engine;
     const uint64_t addr = reinterpret_cast<uint64_t>(dptr);
     const uint64_t row = 32ull * (32 / isz);
     const uint64_t head = std::min<uint64_t>(count, ((32 - addr % 32) % 32) / isz);
@@ -314,7 +325,7 @@ bcn_status validate_enums(int fmt, int layout, int method, int engine) {
     if (fmt < 0 || fmt > 2) return fail(BCN_ERR_INVALID_ARGUMENT, "fill: unknown format");
     if (layout < 0 || layout > 1) return fail(BCN_ERR_INVALID_ARGUMENT, "fill: unknown layout");
     if (method < 0 || method > 3) return fail(BCN_ERR_INVALID_ARGUMENT, "fill: unknown method");
-    if (engine < 0 || engine > 4) return fail(BCN_ERR_INVALID_ARGUMENT, "fill: unknown engine");
+    if (engine < 0 || engine > 5) return fail(BCN_ERR_INVALID_ARGUMENT, "fill: unknown engine");
     return BCN_OK;
 }
 
@@ -456,6 +467,7 @@ const char* bcn_engine_name(int engine) {
         case BCN_ENGINE_MONTGOMERY: return "montgomery";
         case BCN_ENGINE_FP64: return "fp64";
         case BCN_ENGINE_STAGED: return "staged";
+        case BCN_ENGINE_BULK: return "bulk";
     }
     return "?";
 }

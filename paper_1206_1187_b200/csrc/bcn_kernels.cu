@@ -334,6 +334,97 @@ __global__ void __launch_bounds__(kStagedThreads) k_fill_staged(const StagedArgs
     if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// ------------------------------------------------- bulk (TMA) jump fill
+// Jump-stream generation staged through shared memory and written with one
+// TMA bulk store (cp.async.bulk, SASS UBLKCP) per 16 KiB tile. Each CTA owns
+// a contiguous row range; warp w produces rows w and w+8 of every 16-row
+// tile, so each of its streams advances by 16 rows per tile (one multiplier).
+// Within a row a lane owns two 16-byte chunks (c*512 + lane*16 bytes), which
+// makes both smem stores of the warp conflict-free.
+template <int FMT, int ENG>
+__global__ void __launch_bounds__(kContigThreads) k_fill_bulk(const ContigArgs a) {
+    using E = Eng<ENG>;
+    using Item = typename Fmt<FMT>::Item;
+    constexpr int EPC = 16 / sizeof(Item);           // elements per 16-byte chunk
+    constexpr uint64_t ROW = 1024 / sizeof(Item);    // elements per 1 KiB row
+    constexpr uint32_t TILE_ROWS = kBulkTileRows;    // 16
+    constexpr uint32_t TILE_BYTES = TILE_ROWS * 1024;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+    uint64_t r0, r1;  // this CTA's rows
+    {
+        const uint64_t q = a.rows / gridDim.x, rem = a.rows % gridDim.x;
+        r0 = blockIdx.x * q + (blockIdx.x < rem ? blockIdx.x : rem);
+        r1 = r0 + q + (blockIdx.x < rem ? 1 : 0);
+    }
+    if (r0 >= r1) return;
+    // States: [h][c][j] for rows r0 + warp + 8h, chunk c, element j.
+    typename E::State st[2][2][EPC];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const uint64_t j0 = (r0 + warp + 8 * h) * ROW + c * (32 * EPC) + lane * EPC;
+            uint64_t z = dev_state_from_exp(dev_exp_at(a.e0, j0));
+#pragma unroll
+            for (int j = 0; j < EPC; ++j) {
+                st[h][c][j] = E::from_canonical(z);
+                if (j + 1 < EPC) z = step_modified_barrett(z);
+            }
+        }
+    const Mult k = a.jump_row;  // 2^(53 * 16 rows) mod m for this kernel
+    char* gout = static_cast<char*>(a.out);
+    uint32_t it = 0;
+    for (uint64_t t0 = r0; t0 < r1; t0 += TILE_ROWS, ++it) {
+        const uint32_t b = it % kBulkStages;
+        unsigned char* tile = smem_raw + b * TILE_BYTES;
+        if (it >= kBulkStages && threadIdx.x == 0)
+            asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kBulkStages - 1) : "memory");
+        __syncthreads();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t row = warp + 8 * h;
+            if (t0 + row < r1) {
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    uint64_t bits[EPC];
+#pragma unroll
+                    for (int j = 0; j < EPC; ++j) bits[j] = emit_bits<FMT, E>(st[h][c][j]);
+                    uint64_t w0, w1;
+                    if constexpr (EPC == 2) {
+                        w0 = bits[0];
+                        w1 = bits[1];
+                    } else {
+                        w0 = bits[0] | (bits[1] << 32);
+                        w1 = bits[2] | (bits[3] << 32);
+                    }
+                    const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(
+                        tile + row * 1024 + c * 512 + lane * 16));
+                    asm volatile("st.shared.v2.b64 [%0], {%1, %2};" ::"r"(sa), "l"(w0), "l"(w1)
+                                 : "memory");
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+#pragma unroll
+                for (int j = 0; j < EPC; ++j) st[h][c][j] = E::mul(st[h][c][j], k);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const uint64_t nrows = r1 - t0 < TILE_ROWS ? r1 - t0 : TILE_ROWS;
+            const uint32_t src = static_cast<uint32_t>(__cvta_generic_to_shared(tile));
+            asm volatile(
+                "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n\t"
+                "cp.async.bulk.commit_group;" ::"l"(gout + t0 * 1024),
+                "r"(src), "r"(static_cast<uint32_t>(nrows * 1024))
+                : "memory");
+        }
+    }
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // -------------------------------------------------------- seed / walks
 // SeedArgs.steps == 0: out[t] = state_at(a[t], k[t]) (generator.cpp:42-49).
 // steps > 0: out[t*steps + s] = the (s+1)-th next() from that state.
@@ -533,6 +624,37 @@ cudaError_t launch_staged(int fmt, const StagedArgs& a, int grid, cudaStream_t s
             return cudaErrorInvalidValue;
     }
     return counted(cudaGetLastError());
+}
+
+cudaError_t launch_bulk(int fmt, const ContigArgs& a, int grid, cudaStream_t s) {
+    const int smem = kBulkStages * kBulkTileRows * 1024;
+    switch (fmt) {
+        case kFmtU64:
+            cudaFuncSetAttribute(k_fill_bulk<kFmtU64, kEngFP64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            k_fill_bulk<kFmtU64, kEngFP64><<<grid, kContigThreads, smem, s>>>(a);
+            break;
+        case kFmtF64:
+            cudaFuncSetAttribute(k_fill_bulk<kFmtF64, kEngFP64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            k_fill_bulk<kFmtF64, kEngFP64><<<grid, kContigThreads, smem, s>>>(a);
+            break;
+        case kFmtF32:
+            cudaFuncSetAttribute(k_fill_bulk<kFmtF32, kEngFP64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            k_fill_bulk<kFmtF32, kEngFP64><<<grid, kContigThreads, smem, s>>>(a);
+            break;
+        default:
+            return cudaErrorInvalidValue;
+    }
+    return counted(cudaGetLastError());
+}
+
+int bulk_blocks_per_sm(int fmt) {
+    const size_t smem = static_cast<size_t>(kBulkStages) * kBulkTileRows * 1024;
+    switch (fmt) {
+        case kFmtU64: return occupancy(k_fill_bulk<kFmtU64, kEngFP64>, kContigThreads, smem);
+        case kFmtF64: return occupancy(k_fill_bulk<kFmtF64, kEngFP64>, kContigThreads, smem);
+        case kFmtF32: return occupancy(k_fill_bulk<kFmtF32, kEngFP64>, kContigThreads, smem);
+    }
+    return 1;
 }
 
 cudaError_t launch_seed(const SeedArgs& a, cudaStream_t s) {

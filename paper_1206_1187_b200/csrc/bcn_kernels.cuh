@@ -11,7 +11,14 @@
 namespace bcn_b200 {
 
 enum Format : int { kFmtU64 = 0, kFmtF64 = 1, kFmtF32 = 2 };
-enum Engine : int { kEngAuto = 0, kEngBarrett = 1, kEngMontgomery = 2, kEngFP64 = 3, kEngStaged = 4 };
+enum Engine : int {
+    kEngAuto = 0,
+    kEngBarrett = 1,
+    kEngMontgomery = 2,
+    kEngFP64 = 3,
+    kEngStaged = 4,  // paper T=1 modified-Barrett runs, smem transpose, TMA bulk store
+    kEngBulk = 5     // FP64 jump streams, smem-staged 16 KiB tiles, TMA bulk store
+};
 
 inline int format_itemsize(int fmt) { return fmt == kFmtF32 ? 4 : 8; }
 
@@ -106,6 +113,7 @@ cudaError_t launch_interleaved(int fmt, int engine, const InterleavedArgs& a, in
                                cudaStream_t s);
 cudaError_t launch_slots(int fmt, const SlotArgs& a, cudaStream_t s);
 cudaError_t launch_staged(int fmt, const StagedArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_bulk(int fmt, const ContigArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_seed(const SeedArgs& a, cudaStream_t s);
 cudaError_t launch_digest(const DigestArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_constant(const ConstArgs& a, int grid, int block, cudaStream_t s);
@@ -120,9 +128,12 @@ cudaError_t upload_tables();
 // Resident CTAs per SM for the contiguous kernel of (fmt, engine) at `block`.
 int contig_blocks_per_sm(int fmt, int engine, int block);
 int interleaved_blocks_per_sm(int fmt, int engine, int block);
+int bulk_blocks_per_sm(int fmt);
 
 constexpr int kStagedL = 15;          // odd: conflict-free strided smem stores
 constexpr int kStagedThreads = 256;
 constexpr int kContigThreads = 256;
+constexpr int kBulkTileRows = 16;  // 16 KiB per TMA bulk store
+constexpr int kBulkStages = 3;     // tiles in flight per CTA
 
 }  // namespace bcn_b200

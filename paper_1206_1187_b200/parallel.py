@@ -51,6 +51,7 @@ class Engine(enum.IntEnum):
     Montgomery = 2
     FP64 = 3
     Staged = 4
+    Bulk = 5
 
 
 def layout_name(layout: Layout) -> str:

@@ -15,7 +15,7 @@ import oracle as O
 pytestmark = pytest.mark.gpu
 
 A0 = O.MIN_SEED
-ENGINES = ["Barrett", "Montgomery", "FP64", "Staged"]
+ENGINES = ["Barrett", "Montgomery", "FP64", "Staged", "Bulk"]
 FORMATS = [(O.FMT_U64, torch.int64, np.uint64), (O.FMT_F64, torch.float64, np.float64),
            (O.FMT_F32, torch.float32, np.float32)]
 
