@@ -149,6 +149,21 @@ int bcn_auto_engine(bcn_format format);
  * their own launches inside a timed region with it). */
 uint64_t bcn_launch_count(void);
 
+/* Process-wide launch tuning of the contiguous fill and Constant kernels:
+ * CTAs per SM of the persistent grid (0 = as many as fit) and row order
+ * (0 = per-warp contiguous row ranges, 1 = grid-strided rows, the default).
+ * Output bits never depend on it. */
+bcn_status bcn_set_launch_config(int ctas_per_sm, int row_order);
+
+/* Process-wide HBM write pacing of the contiguous fill and Constant kernels.
+ * B200 write efficiency drops when SM stores oversubscribe HBM; the paced
+ * kernels meter their stores to `target_gbs` (GB/s, per device) with one pacer
+ * warp per CTA reading %globaltimer. 0 disables pacing. ctas_per_sm in [1,7].
+ * Output bits never depend on it. */
+bcn_status bcn_set_write_pacing(double target_gbs, int ctas_per_sm);
+/* Current pacing target in GB/s (0 = unpaced). */
+double bcn_write_pacing(void);
+
 #ifdef __cplusplus
 }
 #endif

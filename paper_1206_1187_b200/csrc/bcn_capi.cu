@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <cstring>
 #include <map>
@@ -131,8 +132,25 @@ int blocks_per_sm(DevCtx* c, int fmt, int engine, bool interleaved) {
     return n;
 }
 
+// Launch tuning (bcn_set_launch_config): CTAs per SM for the persistent
+// fill grids (0 = as many as fit) and the row order of the contiguous kernels.
+std::atomic<int> g_ctas_per_sm{0};
+std::atomic<int> g_row_order{1};
+// Write pacing (bcn_set_write_pacing): target HBM write rate of the paced
+// contiguous kernels in GB/s (0 = unpaced) and their CTAs per SM.
+std::atomic<double> g_pace_gbs{kDefaultPaceGBs};
+std::atomic<int> g_pace_cps{2};
+
+uint64_t pace_gap_q8(int grid, double gbs) {
+    // One CTA round writes grid * 8 rows * 1 KiB; 1 GB/s == 1 byte/ns.
+    return static_cast<uint64_t>(256.0 * grid * (kPacedThreads / 32 - 1) * 1024.0 / gbs);
+}
+
 int grid_for_rows(DevCtx* c, int fmt, int engine, bool interleaved, uint64_t rows) {
-    const uint64_t persistent = static_cast<uint64_t>(c->sms) * blocks_per_sm(c, fmt, engine, interleaved);
+    int per_sm = blocks_per_sm(c, fmt, engine, interleaved);
+    const int want = g_ctas_per_sm.load();
+    if (want > 0 && want < per_sm) per_sm = want;
+    const uint64_t persistent = static_cast<uint64_t>(c->sms) * per_sm;
     const uint64_t needed = (rows + (kContigThreads / 32) - 1) / (kContigThreads / 32);
     return static_cast<int>(std::max<uint64_t>(1, std::min(persistent, needed)));
 }
@@ -219,9 +237,24 @@ cudaError_t enqueue_affine(const FillJob& j, char* dptr, uint64_t slot0, uint64_
             const uint64_t persistent = static_cast<uint64_t>(j.ctx->sms) * bulk_blocks_per_sm(j.fmt);
             const int grid = static_cast<int>(std::max<uint64_t>(1, std::min(persistent, tiles)));
             e = launch_bulk(j.fmt, c, grid, j.stream);
+        } else if (g_pace_gbs.load() > 0.0 && isz == 8) {
+            // Paced path (8-byte formats; f32 is FP64-pipe bound below the
+            // write roof, where metering cannot help).
+            constexpr uint64_t kWorkers = kPacedThreads / 32 - 1;
+            const uint64_t want = static_cast<uint64_t>(j.ctx->sms) * g_pace_cps.load();
+            const int grid = static_cast<int>(std::max<uint64_t>(1, std::min(want, (rows + kWorkers - 1) / kWorkers)));
+            PacedArgs pa;
+            pa.out = c.out;
+            pa.rows = rows;
+            pa.e0 = c.e0;
+            pa.jump = mult_for_steps(static_cast<__int128>(row) * grid * kWorkers);
+            pa.gap_q8 = pace_gap_q8(grid, g_pace_gbs.load());
+            e = launch_paced(j.fmt, j.engine, pa, grid, j.stream);
         } else {
-            c.jump_row = mult_for_steps(static_cast<__int128>(row));
             const int grid = grid_for_rows(j.ctx, j.fmt, j.engine, false, rows);
+            c.stride_order = static_cast<uint32_t>(g_row_order.load());
+            const uint64_t step_rows = c.stride_order ? static_cast<uint64_t>(grid) * (kContigThreads / 32) : 1;
+            c.jump_row = mult_for_steps(static_cast<__int128>(row) * step_rows);
             e = launch_contig(j.fmt, j.engine, c, grid, kContigThreads, j.stream);
         }
         if (e != cudaSuccess) return e;
@@ -485,6 +518,24 @@ int bcn_auto_engine(bcn_format format) { return resolve_engine(kEngAuto, format)
 
 uint64_t bcn_launch_count(void) { return launch_count(); }
 
+bcn_status bcn_set_write_pacing(double target_gbs, int ctas_per_sm) {
+    if (!(target_gbs >= 0.0) || target_gbs > 1e5 || ctas_per_sm < 1 || ctas_per_sm > 7)
+        return fail(BCN_ERR_INVALID_ARGUMENT, "set_write_pacing: target_gbs >= 0, ctas_per_sm in [1,7]");
+    g_pace_gbs.store(target_gbs);
+    g_pace_cps.store(ctas_per_sm);
+    return BCN_OK;
+}
+
+double bcn_write_pacing(void) { return g_pace_gbs.load(); }
+
+bcn_status bcn_set_launch_config(int ctas_per_sm, int row_order) {
+    if (ctas_per_sm < 0 || ctas_per_sm > 32 || row_order < 0 || row_order > 1)
+        return fail(BCN_ERR_INVALID_ARGUMENT, "set_launch_config: ctas_per_sm in [0,32], row_order 0|1");
+    g_ctas_per_sm.store(ctas_per_sm);
+    g_row_order.store(row_order);
+    return BCN_OK;
+}
+
 bcn_status bcn_modpow2(uint64_t e, uint64_t modulus, uint64_t* out) {
     // generator.cpp:17-30
     if (!out) return fail(BCN_ERR_INVALID_ARGUMENT, "modpow2: null output");
@@ -735,9 +786,20 @@ bcn_status bcn_fill_constant(void* out, uint64_t nbytes, uint64_t pattern, int d
     DevCtx* c = nullptr;
     if ((st = get_ctx(dev, &c))) return st;
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->stream;
-    ConstArgs ca{out, nbytes / 1024, pattern};
-    const int grid = grid_for_rows(c, kFmtF64, kEngBarrett, false, ca.rows);
-    cudaError_t e = launch_constant(ca, grid, kContigThreads, s);
+    cudaError_t e;
+    if (g_pace_gbs.load() > 0.0) {
+        // The Constant writer under the same metering as the paced fill.
+        constexpr uint64_t kWorkers = kPacedThreads / 32 - 1;
+        const uint64_t rows = nbytes / 1024;
+        const uint64_t want = static_cast<uint64_t>(c->sms) * g_pace_cps.load();
+        const int grid = static_cast<int>(std::max<uint64_t>(1, std::min(want, (rows + kWorkers - 1) / kWorkers)));
+        PacedArgs pa{out, rows, pattern, Mult{}, pace_gap_q8(grid, g_pace_gbs.load())};
+        e = launch_paced(kFmtU64, -1, pa, grid, s);
+    } else {
+        ConstArgs ca{out, nbytes / 1024, pattern, static_cast<uint32_t>(g_row_order.load())};
+        const int grid = grid_for_rows(c, kFmtF64, kEngBarrett, false, ca.rows);
+        e = launch_constant(ca, grid, kContigThreads, s);
+    }
     if (e != cudaSuccess) return cuda_fail(e, "fill_constant launch");
     if (!stream) BCN_CUDA(cudaStreamSynchronize(s));
     return BCN_OK;

@@ -167,8 +167,18 @@ __global__ void __launch_bounds__(kContigThreads) k_fill_contig(const ContigArgs
     const unsigned lane = threadIdx.x & 31;
     const uint64_t nw = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
     const uint64_t w = static_cast<uint64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    uint64_t r, r_end;
-    warp_rows(a.rows, nw, w, r, r_end);
+    // Row order: contiguous per-warp ranges, or grid-strided (warp w writes rows
+    // w, w+nw, ...; all warps sweep the buffer together, which keeps the DRAM
+    // write stream local). jump_row advances a stream by `step` rows.
+    uint64_t r, r_end, step;
+    if (a.stride_order) {
+        r = w;
+        r_end = a.rows;
+        step = nw;
+    } else {
+        warp_rows(a.rows, nw, w, r, r_end);
+        step = 1;
+    }
     if (r >= r_end) return;
 
     // Seed: one windowed power per lane, then T=1 steps for the lane's vector.
@@ -184,15 +194,97 @@ __global__ void __launch_bounds__(kContigThreads) k_fill_contig(const ContigArgs
     const Mult k = a.jump_row;
     char* p = static_cast<char*>(a.out) + (r * ROW + lane * V) * sizeof(typename Fmt<FMT>::Item);
     constexpr uint64_t kRowBytes = ROW * sizeof(typename Fmt<FMT>::Item);
+    const uint64_t pstep = step * kRowBytes;
 #pragma unroll 2
-    for (; r < r_end; ++r) {
+    for (; r < r_end; r += step) {
         uint64_t bits[V];
 #pragma unroll
         for (int v = 0; v < V; ++v) bits[v] = emit_bits<FMT, E>(st[v]);
         pack_store<FMT>(p, bits);
 #pragma unroll
         for (int v = 0; v < V; ++v) st[v] = E::mul(st[v], k);
-        p += kRowBytes;
+        p += pstep;
+    }
+}
+
+// ------------------------------------------------------- paced contiguous fill
+// HBM write efficiency on B200 collapses when SM stores oversubscribe the
+// memory system (measured: ~6.3-6.4 TB/s back-to-back vs ~7.3-7.5 TB/s when
+// the offered load is held just under capacity; profiles/r01/write_probe*.jsonl).
+// This variant meters its own stores in real time: each CTA has 8 worker warps
+// and one pacer warp. Workers generate their next 1 KiB row while the pacer
+// waits on %globaltimer; every `gap` ns the pacer releases named barrier 1 and
+// each worker stores the row it has ready. Rows are grid-strided (worker w of
+// nwk writes rows w, w+nwk, ...), so the whole grid sweeps the buffer as one
+// ordered stream at the target rate. With CONST the worker stores a fixed
+// pattern (the paced Constant writer).
+__device__ __forceinline__ uint64_t global_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+template <int FMT, int ENG, bool CONST>
+__global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a) {
+    using E = Eng<ENG>;
+    constexpr int V = Fmt<FMT>::kVec;
+    constexpr uint64_t ROW = 32ull * V;
+    constexpr int kWorkers = kPacedThreads / 32 - 1;
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t nwk = static_cast<uint64_t>(gridDim.x) * kWorkers;
+    const uint64_t first = static_cast<uint64_t>(blockIdx.x) * kWorkers;
+    const uint64_t rounds = a.rows > first ? (a.rows - first + nwk - 1) / nwk : 0;
+    if (rounds == 0) return;  // uniform across the CTA
+    if (warp == kWorkers) {
+        // Pacer: release round k no earlier than t0 + k * gap.
+        uint64_t t0 = 0;
+        if (lane == 0) t0 = global_ns();
+        for (uint64_t k = 0; k < rounds; ++k) {
+            if (lane == 0 && a.gap_q8) {
+                const uint64_t target = t0 + ((k * a.gap_q8) >> 8);
+                uint64_t now = global_ns();
+                while (now < target) {
+                    const uint64_t d = target - now;
+                    __nanosleep(d > 2048 ? 1024u : static_cast<unsigned>(d >> 1));
+                    now = global_ns();
+                }
+            }
+            __syncwarp();
+            asm volatile("bar.sync 1, %0;" ::"n"(kPacedThreads) : "memory");
+        }
+        return;
+    }
+    const uint64_t w = first + warp;
+    const uint64_t count = a.rows > w ? (a.rows - w + nwk - 1) / nwk : 0;
+    typename E::State st[V];
+    if (!CONST && count) {
+        uint64_t z = dev_state_from_exp(dev_exp_at(a.e0, w * ROW + lane * V));
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            st[v] = E::from_canonical(z);
+            if (v + 1 < V) z = step_modified_barrett(z);
+        }
+    }
+    constexpr uint64_t kRowBytes = ROW * sizeof(typename Fmt<FMT>::Item);
+    char* p = static_cast<char*>(a.out) + w * kRowBytes + lane * 32;
+    const uint64_t pstep = nwk * kRowBytes;
+    const Mult k = a.jump;
+    for (uint64_t r = 0; r < rounds; ++r) {
+        uint64_t bits[V];
+        if (CONST) {
+#pragma unroll
+            for (int v = 0; v < V; ++v) bits[v] = a.e0;
+        } else {
+#pragma unroll
+            for (int v = 0; v < V; ++v) bits[v] = emit_bits<FMT, E>(st[v]);
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kPacedThreads) : "memory");
+        if (r < count) pack_store<FMT>(p, bits);
+        if (!CONST) {
+#pragma unroll
+            for (int v = 0; v < V; ++v) st[v] = E::mul(st[v], k);
+        }
+        p += pstep;
     }
 }
 
@@ -292,7 +384,7 @@ __global__ void __launch_bounds__(kStagedThreads) k_fill_staged(const StagedArgs
     constexpr int L = kStagedL;
     constexpr uint32_t TILE = kStagedThreads * L;
     constexpr uint32_t TILE_BYTES = TILE * sizeof(Item);
-    extern __shared__ __align__(128) unsigned char smem_raw[];
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
     const unsigned tid = threadIdx.x;
     uint64_t tile = blockIdx.x;
     if (tile >= a.tiles) return;
@@ -483,12 +575,19 @@ __global__ void __launch_bounds__(kContigThreads) k_constant(const ConstArgs a) 
     const unsigned lane = threadIdx.x & 31;
     const uint64_t nw = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
     const uint64_t w = static_cast<uint64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    uint64_t r, r_end;
-    warp_rows(a.rows, nw, w, r, r_end);
+    uint64_t r, r_end, step;
+    if (a.stride_order) {
+        r = w;
+        r_end = a.rows;
+        step = nw;
+    } else {
+        warp_rows(a.rows, nw, w, r, r_end);
+        step = 1;
+    }
     const uint64_t v[4] = {a.value, a.value, a.value, a.value};
     char* p = static_cast<char*>(a.out) + r * 1024 + lane * 32;
 #pragma unroll 4
-    for (; r < r_end; ++r, p += 1024) st256(p, v);
+    for (; r < r_end; r += step, p += step * 1024) st256(p, v);
 }
 
 // ------------------------------------------------------------ transpose
@@ -576,6 +675,29 @@ cudaError_t launch_contig(int fmt, int engine, const ContigArgs& a, int grid, in
         case kFmtU64: return contig_fmt<kFmtU64>(engine, a, grid, block, s);
         case kFmtF64: return contig_fmt<kFmtF64>(engine, a, grid, block, s);
         case kFmtF32: return contig_fmt<kFmtF32>(engine, a, grid, block, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+namespace {
+template <int FMT>
+cudaError_t paced_fmt(int engine, const PacedArgs& a, int grid, cudaStream_t s) {
+    switch (engine) {
+        case kEngBarrett: k_fill_paced<FMT, kEngBarrett, false><<<grid, kPacedThreads, 0, s>>>(a); break;
+        case kEngMontgomery: k_fill_paced<FMT, kEngMontgomery, false><<<grid, kPacedThreads, 0, s>>>(a); break;
+        case kEngFP64: k_fill_paced<FMT, kEngFP64, false><<<grid, kPacedThreads, 0, s>>>(a); break;
+        case -1: k_fill_paced<FMT, kEngBarrett, true><<<grid, kPacedThreads, 0, s>>>(a); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return counted(cudaGetLastError());
+}
+}  // namespace
+
+cudaError_t launch_paced(int fmt, int engine, const PacedArgs& a, int grid, cudaStream_t s) {
+    switch (fmt) {
+        case kFmtU64: return paced_fmt<kFmtU64>(engine, a, grid, s);
+        case kFmtF64: return paced_fmt<kFmtF64>(engine, a, grid, s);
+        case kFmtF32: return paced_fmt<kFmtF32>(engine, a, grid, s);
     }
     return cudaErrorInvalidValue;
 }

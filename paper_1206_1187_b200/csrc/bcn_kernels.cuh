@@ -28,7 +28,18 @@ struct ContigArgs {
     void* out;
     uint64_t rows;
     uint64_t e0;
-    Mult jump_row;  // 2^(53 * elements_per_row) mod m
+    Mult jump_row;          // 2^(53 * elements per stream step) mod m
+    uint32_t stride_order;  // 0: per-warp row ranges; 1: grid-strided rows
+};
+
+// Paced contiguous fill (k_fill_paced): grid-strided rows metered to a
+// target HBM write rate by one pacer warp per CTA.
+struct PacedArgs {
+    void* out;        // 32-byte aligned
+    uint64_t rows;    // rows of 32 lanes x 32 bytes
+    uint64_t e0;      // exponent of element 0 (or the 8-byte pattern, Constant)
+    Mult jump;        // 2^(53 * nwk * ROW) mod m, nwk = grid * 8 worker warps
+    uint64_t gap_q8;  // ns between CTA rounds, x256 (0 = unpaced)
 };
 
 // Interleaved region fast path (reference Layout::Interleaved,
@@ -93,6 +104,7 @@ struct ConstArgs {
     void* out;
     uint64_t rows;  // rows of 32 lanes x 32 bytes
     uint64_t value; // bit pattern replicated (8 bytes)
+    uint32_t stride_order;
 };
 
 struct TransposeArgs {
@@ -111,6 +123,8 @@ cudaError_t launch_contig(int fmt, int engine, const ContigArgs& a, int grid, in
                           cudaStream_t s);
 cudaError_t launch_interleaved(int fmt, int engine, const InterleavedArgs& a, int grid, int block,
                                cudaStream_t s);
+// engine -1 = paced Constant writer (pattern in a.e0)
+cudaError_t launch_paced(int fmt, int engine, const PacedArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_slots(int fmt, const SlotArgs& a, cudaStream_t s);
 cudaError_t launch_staged(int fmt, const StagedArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_bulk(int fmt, const ContigArgs& a, int grid, cudaStream_t s);
@@ -133,6 +147,11 @@ int bulk_blocks_per_sm(int fmt);
 constexpr int kStagedL = 15;          // odd: conflict-free strided smem stores
 constexpr int kStagedThreads = 256;
 constexpr int kContigThreads = 256;
+constexpr int kPacedThreads = 288;  // 8 worker warps + 1 pacer warp
+// Measured default pacing target for the 8-byte formats (DESIGN.md §5,
+// profiles/r01/tune_pace.jsonl): FP64 engine f64/u64 reach ~7.08 TB/s at
+// 7200 vs ~6.25 unpaced; above ~7.3 the write path starts to oversubscribe.
+constexpr double kDefaultPaceGBs = 7200.0;
 constexpr int kBulkTileRows = 16;  // 16 KiB per TMA bulk store
 constexpr int kBulkStages = 3;     // tiles in flight per CTA
 

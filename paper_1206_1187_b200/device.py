@@ -74,6 +74,22 @@ def fill_multi(outs: list[torch.Tensor], n: int, seed_index: int = kMinSeedIndex
               base_offset & 0xFFFFFFFFFFFFFFFF, int(engine))
 
 
+def set_launch_config(ctas_per_sm: int = 0, row_order: int = 1) -> None:
+    """Process-wide CTAs-per-SM / row-order tuning of the contiguous kernels
+    (bits never change; see bcn_set_launch_config)."""
+    _lib.call("bcn_set_launch_config", ctas_per_sm, row_order)
+
+
+def set_write_pacing(target_gbs: float, ctas_per_sm: int = 2) -> None:
+    """Meter the contiguous fill / Constant stores to `target_gbs` per device
+    (0 = unpaced); see bcn_set_write_pacing."""
+    _lib.call("bcn_set_write_pacing", float(target_gbs), ctas_per_sm)
+
+
+def write_pacing() -> float:
+    return float(_lib.lib().bcn_write_pacing())
+
+
 def auto_engine(fmt: Format = Format.F64) -> Engine:
     return Engine(_lib.lib().bcn_auto_engine(int(fmt)))
 

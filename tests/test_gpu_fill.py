@@ -165,6 +165,26 @@ def test_seed_extremes(bcn, cuda, oracle):
                                                   base_offset=seed % 1000003))
 
 
+@pytest.mark.parametrize("pace", [7000.0, 1e5])
+def test_paced_kernels_bit_exact(bcn, cuda, oracle, pace):
+    """The write-paced contiguous kernels (pacer warp + named barrier) produce
+    the same bits as every other path, for all engines and formats."""
+    old = bcn.device.write_pacing()
+    try:
+        bcn.device.set_write_pacing(pace, 2)
+        for engine in ("Barrett", "Montgomery", "FP64"):
+            for fmt in (O.FMT_U64, O.FMT_F64, O.FMT_F32):
+                n = 2**20 + 4099
+                got = dev_fill(bcn, n, fmt, engine=engine, base=777, offset=1)
+                assert np.array_equal(bits(got), bits(oracle.fill(n, fmt, base_offset=777)))
+        c = torch.empty(1 << 20, dtype=torch.float64, device=cuda)
+        bcn.device.fill_constant(c)
+        torch.cuda.synchronize()
+        assert bool((c == 0.5).all())
+    finally:
+        bcn.device.set_write_pacing(old, 2)
+
+
 # ------------------------------------------------------------- host buffers
 def test_host_numpy_output_chunked(bcn, cuda, oracle):
     """Host (pageable) span like the reference's std::span fill: > one 64 MiB chunk."""
