@@ -182,7 +182,7 @@ ENGINE_NAMES = {"auto": "Auto", "barrett": "Barrett", "montgomery": "Montgomery"
 def kernel_name(fmt: int, engine: int, paced: bool) -> str:
     """Template instance name of the dominant kernel for (format, engine)."""
     if paced and fmt != 2 and engine in (1, 2, 3):
-        return f"void k_fill_paced<{fmt}, {engine}, false>(PacedArgs)"
+        return f"void k_fill_paced<{fmt}, {engine}, 0>(PacedArgs)"
     if engine == 4:
         return f"void k_fill_staged<{fmt}>(StagedArgs)"
     if engine == 5:
