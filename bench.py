@@ -293,10 +293,10 @@ def main() -> None:
                             max(20, args.steps // 4), 5)
     const_gbs = buf_items * isz / (statistics.mean(const_per) * 1e-3) / 1e9
     pace_now = lib.bcn_write_pacing()
-    lib.bcn_set_write_pacing(0.0, 2)
+    lib.bcn_set_write_pacing(0.0, 2, 3)
     const_per_u, _, _ = timed(lambda: B.device.fill_constant(raw, stream=stream),
                               max(20, args.steps // 4), 5)
-    lib.bcn_set_write_pacing(pace_now, 2)
+    lib.bcn_set_write_pacing(pace_now, 2, 3)
     const_unpaced_gbs = buf_items * isz / (statistics.mean(const_per_u) * 1e-3) / 1e9
 
     # Headline: device-resident fill, every step writes this rank's whole share.

@@ -64,14 +64,15 @@ typedef enum bcn_engine {
     BCN_ENGINE_MONTGOMERY = 2, /* Montgomery REDC jump multiply            */
     BCN_ENGINE_FP64 = 3,       /* exact FP64-pipe jump multiply            */
     BCN_ENGINE_STAGED = 4,     /* paper T=1 modified Barrett + TMA bulk store */
-    BCN_ENGINE_BULK = 5        /* FP64 jump streams staged in smem + TMA bulk store */
+    BCN_ENGINE_BULK = 5,       /* FP64 jump streams staged in smem + TMA bulk store */
+    BCN_ENGINE_MIXED = 6       /* DFMA quotient + exact integer remainder   */
 } bcn_engine;
 
 /* ---- library ---------------------------------------------------------- */
 int bcn_abi_version(void);
 /* Message for the calling thread's most recent non-OK status ("" if none). */
 const char* bcn_last_error(void);
-/* Name of an engine ("auto", "barrett", "montgomery", "fp64", "staged", "bulk"). */
+/* Name of an engine ("auto", "barrett", "montgomery", "fp64", "staged", "bulk", "mixed"). */
 const char* bcn_engine_name(int engine);
 /* Number of visible CUDA devices (0 when none; never an error). */
 int bcn_device_count(void);
@@ -158,9 +159,10 @@ bcn_status bcn_set_launch_config(int ctas_per_sm, int row_order);
 /* Process-wide HBM write pacing of the contiguous fill and Constant kernels.
  * B200 write efficiency drops when SM stores oversubscribe HBM; the paced
  * kernels meter their stores to `target_gbs` (GB/s, per device) with one pacer
- * warp per CTA reading %globaltimer. 0 disables pacing. ctas_per_sm in [1,7].
+ * warp per CTA reading %globaltimer. 0 disables pacing. ctas_per_sm in [1,7];
+ * format_mask: bit f enables pacing for bcn_format f (default U64|F64 = 3).
  * Output bits never depend on it. */
-bcn_status bcn_set_write_pacing(double target_gbs, int ctas_per_sm);
+bcn_status bcn_set_write_pacing(double target_gbs, int ctas_per_sm, int format_mask);
 /* Current pacing target in GB/s (0 = unpaced). */
 double bcn_write_pacing(void);
 

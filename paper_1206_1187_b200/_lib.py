@@ -31,7 +31,7 @@ SIGNATURES = [
     ("bcn_auto_engine", _int, [_int]),
     ("bcn_launch_count", _u64, []),
     ("bcn_set_launch_config", _int, [_int, _int]),
-    ("bcn_set_write_pacing", _int, [ctypes.c_double, _int]),
+    ("bcn_set_write_pacing", _int, [ctypes.c_double, _int, _int]),
     ("bcn_write_pacing", ctypes.c_double, []),
     ("bcn_modpow2", _int, [_u64, _u64, _pu64]),
     ("bcn_seed_from_index", _int, [_u64, _pu64]),

@@ -140,6 +140,7 @@ std::atomic<int> g_row_order{1};
 // contiguous kernels in GB/s (0 = unpaced) and their CTAs per SM.
 std::atomic<double> g_pace_gbs{kDefaultPaceGBs};
 std::atomic<int> g_pace_cps{2};
+std::atomic<int> g_pace_formats{(1 << kFmtU64) | (1 << kFmtF64)};
 
 uint64_t pace_gap_q8(int grid, double gbs) {
     // One CTA round writes grid * 8 rows * 1 KiB; 1 GB/s == 1 byte/ns.
@@ -237,9 +238,9 @@ cudaError_t enqueue_affine(const FillJob& j, char* dptr, uint64_t slot0, uint64_
             const uint64_t persistent = static_cast<uint64_t>(j.ctx->sms) * bulk_blocks_per_sm(j.fmt);
             const int grid = static_cast<int>(std::max<uint64_t>(1, std::min(persistent, tiles)));
             e = launch_bulk(j.fmt, c, grid, j.stream);
-        } else if (g_pace_gbs.load() > 0.0 && isz == 8) {
-            // Paced path (8-byte formats; f32 is FP64-pipe bound below the
-            // write roof, where metering cannot help).
+        } else if (g_pace_gbs.load() > 0.0 && (g_pace_formats.load() >> j.fmt & 1)) {
+            // Paced path (by default for the 8-byte formats; f32 with the
+            // FP64 engine is FP64-pipe bound below the write roof).
             constexpr uint64_t kWorkers = kPacedThreads / 32 - 1;
             const uint64_t want = static_cast<uint64_t>(j.ctx->sms) * g_pace_cps.load();
             const int grid = static_cast<int>(std::max<uint64_t>(1, std::min(want, (rows + kWorkers - 1) / kWorkers)));
@@ -358,7 +359,7 @@ bcn_status validate_enums(int fmt, int layout, int method, int engine) {
     if (fmt < 0 || fmt > 2) return fail(BCN_ERR_INVALID_ARGUMENT, "fill: unknown format");
     if (layout < 0 || layout > 1) return fail(BCN_ERR_INVALID_ARGUMENT, "fill: unknown layout");
     if (method < 0 || method > 3) return fail(BCN_ERR_INVALID_ARGUMENT, "fill: unknown method");
-    if (engine < 0 || engine > 5) return fail(BCN_ERR_INVALID_ARGUMENT, "fill: unknown engine");
+    if (engine < 0 || engine > 6) return fail(BCN_ERR_INVALID_ARGUMENT, "fill: unknown engine");
     return BCN_OK;
 }
 
@@ -501,6 +502,7 @@ const char* bcn_engine_name(int engine) {
         case BCN_ENGINE_FP64: return "fp64";
         case BCN_ENGINE_STAGED: return "staged";
         case BCN_ENGINE_BULK: return "bulk";
+        case BCN_ENGINE_MIXED: return "mixed";
     }
     return "?";
 }
@@ -518,11 +520,14 @@ int bcn_auto_engine(bcn_format format) { return resolve_engine(kEngAuto, format)
 
 uint64_t bcn_launch_count(void) { return launch_count(); }
 
-bcn_status bcn_set_write_pacing(double target_gbs, int ctas_per_sm) {
-    if (!(target_gbs >= 0.0) || target_gbs > 1e5 || ctas_per_sm < 1 || ctas_per_sm > 7)
-        return fail(BCN_ERR_INVALID_ARGUMENT, "set_write_pacing: target_gbs >= 0, ctas_per_sm in [1,7]");
+bcn_status bcn_set_write_pacing(double target_gbs, int ctas_per_sm, int format_mask) {
+    if (!(target_gbs >= 0.0) || target_gbs > 1e5 || ctas_per_sm < 1 || ctas_per_sm > 7 ||
+        format_mask < 0 || format_mask > 7)
+        return fail(BCN_ERR_INVALID_ARGUMENT,
+                    "set_write_pacing: target_gbs >= 0, ctas_per_sm in [1,7], format_mask in [0,7]");
     g_pace_gbs.store(target_gbs);
     g_pace_cps.store(ctas_per_sm);
+    g_pace_formats.store(format_mask);
     return BCN_OK;
 }
 

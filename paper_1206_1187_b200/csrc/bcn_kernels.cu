@@ -96,6 +96,29 @@ struct Eng<kEngFP64> {
     }
 };
 
+template <>
+struct Eng<kEngMixed> {
+    using State = MixedState;  // balanced integer + its exact double image
+    static __device__ __forceinline__ State from_canonical(uint64_t z) {
+        const int64_t b = z > kModulus / 2 ? static_cast<int64_t>(z - kModulus) : static_cast<int64_t>(z);
+        return State{b, static_cast<double>(b)};
+    }
+    static __device__ __forceinline__ State mul(State s, const Mult& k) {
+        return mul_mixed(s, k.com, k.cbi);
+    }
+    // Sign mask from the integer's high word: z = s + (s < 0 ? m : 0).
+    static __device__ __forceinline__ uint64_t raw(State s) {
+        const uint64_t mask = static_cast<uint64_t>(s.s >> 63);
+        return static_cast<uint64_t>(s.s) + (mask & kModulus);
+    }
+    static __device__ __forceinline__ double unit(State s) {
+        const uint64_t mask = static_cast<uint64_t>(s.s >> 63);
+        const double add = __longlong_as_double(static_cast<long long>(
+            mask & static_cast<uint64_t>(__double_as_longlong(kModulusD))));
+        return __dmul_rn(__dadd_rn(s.d, add), kInvModulus);
+    }
+};
+
 // --------------------------------------------------------------- formats
 template <int FMT>
 struct Fmt;
@@ -636,6 +659,9 @@ cudaError_t contig_fmt(int engine, const ContigArgs& a, int grid, int block, cud
         case kEngFP64:
             k_fill_contig<FMT, kEngFP64><<<grid, block, 0, s>>>(a);
             break;
+        case kEngMixed:
+            k_fill_contig<FMT, kEngMixed><<<grid, block, 0, s>>>(a);
+            break;
         default:
             return cudaErrorInvalidValue;
     }
@@ -653,6 +679,9 @@ cudaError_t inter_fmt(int engine, const InterleavedArgs& a, int grid, int block,
             break;
         case kEngFP64:
             k_fill_interleaved<FMT, kEngFP64><<<grid, block, 0, s>>>(a);
+            break;
+        case kEngMixed:
+            k_fill_interleaved<FMT, kEngMixed><<<grid, block, 0, s>>>(a);
             break;
         default:
             return cudaErrorInvalidValue;
@@ -686,6 +715,7 @@ cudaError_t paced_fmt(int engine, const PacedArgs& a, int grid, cudaStream_t s) 
         case kEngBarrett: k_fill_paced<FMT, kEngBarrett, false><<<grid, kPacedThreads, 0, s>>>(a); break;
         case kEngMontgomery: k_fill_paced<FMT, kEngMontgomery, false><<<grid, kPacedThreads, 0, s>>>(a); break;
         case kEngFP64: k_fill_paced<FMT, kEngFP64, false><<<grid, kPacedThreads, 0, s>>>(a); break;
+        case kEngMixed: k_fill_paced<FMT, kEngMixed, false><<<grid, kPacedThreads, 0, s>>>(a); break;
         case -1: k_fill_paced<FMT, kEngBarrett, true><<<grid, kPacedThreads, 0, s>>>(a); break;
         default: return cudaErrorInvalidValue;
     }
@@ -814,6 +844,7 @@ int contig_blocks_per_sm(int fmt, int engine, int block) {
         case kEngBarrett: return occupancy(k_fill_contig<F, kEngBarrett>, block);    \
         case kEngMontgomery: return occupancy(k_fill_contig<F, kEngMontgomery>, block); \
         case kEngFP64: return occupancy(k_fill_contig<F, kEngFP64>, block);          \
+        case kEngMixed: return occupancy(k_fill_contig<F, kEngMixed>, block);        \
     }
     switch (fmt) {
         case kFmtU64: BCN_OCC(kFmtU64) break;
@@ -830,6 +861,7 @@ int interleaved_blocks_per_sm(int fmt, int engine, int block) {
         case kEngBarrett: return occupancy(k_fill_interleaved<F, kEngBarrett>, block);    \
         case kEngMontgomery: return occupancy(k_fill_interleaved<F, kEngMontgomery>, block); \
         case kEngFP64: return occupancy(k_fill_interleaved<F, kEngFP64>, block);          \
+        case kEngMixed: return occupancy(k_fill_interleaved<F, kEngMixed>, block);        \
     }
     switch (fmt) {
         case kFmtU64: BCN_OCC(kFmtU64) break;

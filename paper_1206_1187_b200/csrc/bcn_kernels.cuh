@@ -17,7 +17,8 @@ enum Engine : int {
     kEngMontgomery = 2,
     kEngFP64 = 3,
     kEngStaged = 4,  // paper T=1 modified-Barrett runs, smem transpose, TMA bulk store
-    kEngBulk = 5     // FP64 jump streams, smem-staged 16 KiB tiles, TMA bulk store
+    kEngBulk = 5,    // FP64 jump streams, smem-staged 16 KiB tiles, TMA bulk store
+    kEngMixed = 6    // DFMA quotient + integer remainder (fewest FP64 ops)
 };
 
 inline int format_itemsize(int fmt) { return fmt == kFmtF32 ? 4 : 8; }

@@ -84,6 +84,7 @@ struct Mult {
     uint64_t mont;
     double cb;
     double com;
+    int64_t cbi;  // balanced multiplier as an integer (mixed engine)
 };
 
 inline Mult host_make_mult(uint64_t c) {
@@ -95,6 +96,7 @@ inline Mult host_make_mult(uint64_t c) {
                                          : static_cast<int64_t>(c);
     k.cb = static_cast<double>(bal);  // exact: |bal| <= m/2 < 2^52
     k.com = k.cb / kModulusD;         // RN(c_bal / m)
+    k.cbi = bal;
     return k;
 }
 
@@ -142,6 +144,28 @@ __device__ __forceinline__ double mul_fp64(double s, double cb, double com) {
     const double q = __dsub_rn(qm, kMagic);      // exact integer quotient estimate
     const double t = __fma_rn(-q, kModulusD, p); // p - q m, exact (|.| < 2^53)
     return __dadd_rn(t, e);                      // s cb - q m, exact, |.| <= 0.7315 m
+}
+
+// Mixed-pipe exact modular multiply: the quotient comes from ONE DFMA (the
+// same rint(s c_b / m + eta) as mul_fp64, read straight out of the magic
+// constant's significand), the remainder from exact 64-bit integer products:
+//     r = s c_b - q m  (mod 2^64),   q = bits(qm) - bits(MAGIC),
+// with |r| <= 0.7315 m < 2^63, so the two's-complement value IS r (proof as
+// for mul_fp64). The state keeps the integer and its exact
+// double image (one I2F per step). Cost: 1 DFMA + ~7 IMAD/IADD + 1 I2F.
+constexpr uint64_t kMagicBits = 0x4338000000000000ull;  // bits of 1.5 * 2^52
+struct MixedState {
+    int64_t s;
+    double d;
+};
+
+__device__ __forceinline__ MixedState mul_mixed(MixedState x, double com, int64_t cbi) {
+    const double qm = __fma_rn(x.d, com, kMagic);
+    const uint64_t qb = static_cast<uint64_t>(__double_as_longlong(qm));
+    const uint64_t r = static_cast<uint64_t>(x.s) * static_cast<uint64_t>(cbi) -
+                       (qb - kMagicBits) * kModulus;
+    const int64_t rs = static_cast<int64_t>(r);
+    return MixedState{rs, __ll2double_rn(rs)};
 }
 
 // Canonical residue (as an exact double) of a balanced FP64 state.

@@ -80,10 +80,11 @@ def set_launch_config(ctas_per_sm: int = 0, row_order: int = 1) -> None:
     _lib.call("bcn_set_launch_config", ctas_per_sm, row_order)
 
 
-def set_write_pacing(target_gbs: float, ctas_per_sm: int = 2) -> None:
+def set_write_pacing(target_gbs: float, ctas_per_sm: int = 2, format_mask: int = 3) -> None:
     """Meter the contiguous fill / Constant stores to `target_gbs` per device
-    (0 = unpaced); see bcn_set_write_pacing."""
-    _lib.call("bcn_set_write_pacing", float(target_gbs), ctas_per_sm)
+    (0 = unpaced) for the formats in `format_mask` (bit = Format value);
+    see bcn_set_write_pacing."""
+    _lib.call("bcn_set_write_pacing", float(target_gbs), ctas_per_sm, format_mask)
 
 
 def write_pacing() -> float:

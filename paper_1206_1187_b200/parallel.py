@@ -52,6 +52,7 @@ class Engine(enum.IntEnum):
     FP64 = 3
     Staged = 4
     Bulk = 5
+    Mixed = 6
 
 
 def layout_name(layout: Layout) -> str:

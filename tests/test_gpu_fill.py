@@ -15,7 +15,7 @@ import oracle as O
 pytestmark = pytest.mark.gpu
 
 A0 = O.MIN_SEED
-ENGINES = ["Barrett", "Montgomery", "FP64", "Staged", "Bulk"]
+ENGINES = ["Barrett", "Montgomery", "FP64", "Staged", "Bulk", "Mixed"]
 FORMATS = [(O.FMT_U64, torch.int64, np.uint64), (O.FMT_F64, torch.float64, np.float64),
            (O.FMT_F32, torch.float32, np.float32)]
 
@@ -109,7 +109,7 @@ def test_interleaved_ragged_million(bcn, cuda, reference):
     assert np.array_equal(bits(got), bits(reference.fill(10**6, O.FMT_F64, workers=7, layout=1)))
 
 
-@pytest.mark.parametrize("engine", ["Barrett", "Montgomery", "FP64"])
+@pytest.mark.parametrize("engine", ["Barrett", "Montgomery", "FP64", "Mixed"])
 @pytest.mark.parametrize("fmt", [O.FMT_U64, O.FMT_F32])
 def test_interleaved_engines_formats(bcn, cuda, oracle, engine, fmt):
     n = 200003
@@ -171,8 +171,8 @@ def test_paced_kernels_bit_exact(bcn, cuda, oracle, pace):
     the same bits as every other path, for all engines and formats."""
     old = bcn.device.write_pacing()
     try:
-        bcn.device.set_write_pacing(pace, 2)
-        for engine in ("Barrett", "Montgomery", "FP64"):
+        bcn.device.set_write_pacing(pace, 2, 7)
+        for engine in ("Barrett", "Montgomery", "FP64", "Mixed"):
             for fmt in (O.FMT_U64, O.FMT_F64, O.FMT_F32):
                 n = 2**20 + 4099
                 got = dev_fill(bcn, n, fmt, engine=engine, base=777, offset=1)
@@ -182,7 +182,7 @@ def test_paced_kernels_bit_exact(bcn, cuda, oracle, pace):
         torch.cuda.synchronize()
         assert bool((c == 0.5).all())
     finally:
-        bcn.device.set_write_pacing(old, 2)
+        bcn.device.set_write_pacing(old, 2, 3)
 
 
 # ------------------------------------------------------------- host buffers

@@ -25,17 +25,17 @@ import paper_1206_1187_b200 as B  # noqa: E402
 A0 = B.kMinSeedIndex
 CONFIGS = [
     # (name, fmt, engine, pace GB/s, pace cps)
-    ("constant_unpaced", "f64", "Constant", 0, 2),
     ("constant_paced7200", "f64", "Constant", 7200, 2),
-    ("f64_barrett_unpaced", "f64", "Barrett", 0, 2),
-    ("f64_fp64_unpaced", "f64", "FP64", 0, 2),
     ("f64_fp64_paced7200", "f64", "FP64", 7200, 2),
-    ("f64_fp64_paced7000", "f64", "FP64", 7000, 2),
-    ("f64_fp64_paced6800", "f64", "FP64", 6800, 2),
-    ("f64_bulk_unpaced", "f64", "Bulk", 0, 2),
-    ("u64_barrett_unpaced", "u64", "Barrett", 0, 2),
+    ("f64_mixed_paced7200", "f64", "Mixed", 7200, 2),
+    ("f64_mixed_paced7200_cps3", "f64", "Mixed", 7200, 3),
+    ("f64_mixed_unpaced", "f64", "Mixed", 0, 2),
     ("u64_fp64_paced7200", "u64", "FP64", 7200, 2),
+    ("u64_mixed_paced7200", "u64", "Mixed", 7200, 2),
+    ("u64_barrett_unpaced", "u64", "Barrett", 0, 2),
     ("f32_fp64_unpaced", "f32", "FP64", 0, 2),
+    ("f32_mixed_unpaced", "f32", "Mixed", 0, 2),
+    ("f32_mixed_paced7200", "f32", "Mixed", 7200, 2),
 ]
 
 
@@ -55,7 +55,7 @@ def main() -> None:
     for name, fmt, eng, pace, cps in CONFIGS:
         if a.only and a.only not in name:
             continue
-        B.device.set_write_pacing(pace, cps)
+        B.device.set_write_pacing(pace, cps, 7 if fmt == 'f32' else 3)
         buf = f32 if fmt == "f32" else (f64.view(torch.int64) if fmt == "u64" else f64)
         if eng == "Constant":
             fn = lambda: B.device.fill_constant(buf.view(torch.int64), stream=stream)  # noqa: E731
@@ -103,7 +103,7 @@ def main() -> None:
                           "power_w": statistics.mean([s[2] for s in late]),
                           "power_cap": bool(reasons & 0x4), "reasons_mask": reasons}), flush=True)
         time.sleep(1.0)
-    B.device.set_write_pacing(7200, 2)
+    B.device.set_write_pacing(7200, 2, 3)
 
 
 if __name__ == "__main__":

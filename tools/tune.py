@@ -53,7 +53,7 @@ def main() -> None:
         for c in configs:
             fmt, eng, order, cps = c
             if a.pace:
-                B.device.set_write_pacing(order, cps)
+                B.device.set_write_pacing(order, cps, 7)
             else:
                 B.device.set_write_pacing(0, 1)
                 B.device.set_launch_config(cps, order)
