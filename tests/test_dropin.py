@@ -17,6 +17,7 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 DROPIN = os.path.join(ROOT, "tests", "cpp", "build", "test_dropin")
 REFTESTS = os.path.join(ROOT, "oracle", "_ref", "ref_tests_on_b200")
+DEVICE_API = os.path.join(ROOT, "tests", "cpp", "build", "test_device_api")
 
 
 def test_dropin_headers_compile_and_link(bcn):
@@ -25,6 +26,9 @@ def test_dropin_headers_compile_and_link(bcn):
                        capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
     assert os.path.exists(DROPIN)
+    r = subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp"), "device"],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
     if os.path.isdir("/root/reference/proj"):
         r = subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp"), "ref"],
                            capture_output=True, text=True)
@@ -55,3 +59,13 @@ def test_reference_unit_tests_pass_on_the_b200_library(cuda):
         pytest.skip("oracle/_ref/ref_tests_on_b200 not built (needs /root/reference at build time)")
     out = _run(REFTESTS)
     assert "test cases: 23" in out
+
+
+@pytest.mark.gpu
+def test_device_side_api_matches_library_fill(cuda):
+    """include/bcnrand_device.cuh inside a user kernel == bcn_fill, bit for bit."""
+    if not os.path.exists(DEVICE_API):
+        pytest.skip("tests/cpp/build/test_device_api not built")
+    r = subprocess.run([DEVICE_API], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "[device-api] ok" in r.stdout
