@@ -166,6 +166,21 @@ bcn_status bcn_set_write_pacing(double target_gbs, int ctas_per_sm, int format_m
 /* Current pacing target in GB/s (0 = unpaced). */
 double bcn_write_pacing(void);
 
+/* ---- quality.hpp: statistical smoke suite on the GPU ---
+ * Host or device input pointers. Preconditions and formulas follow
+ * quality.cpp:21-118; chi-square and monobit statistics are computed from
+ * exact device counts (bit-identical to the reference), the lag correlation
+ * from per-block partial sums reduced in a fixed order (deterministic). */
+/* quality.hpp:27 — chi-square over `bins` equal bins of (0,1). */
+bcn_status bcn_chi_square_uniformity(const double* samples, uint64_t n, int bins, double* statistic,
+                                     int* dof, int* pass, int device, void* stream);
+/* quality.hpp:33 — worst one-frequency deviation over bits 5..52 of floor(z 2^53/m). */
+bcn_status bcn_monobit_mantissa(const uint64_t* residues, uint64_t n, double* statistic, int* worst_bit,
+                                int* pass, int device, void* stream);
+/* quality.hpp:37 — Pearson correlation of samples `lag` apart. */
+bcn_status bcn_serial_correlation(const double* samples, uint64_t n, int lag, double* rho, int* pass,
+                                  int device, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

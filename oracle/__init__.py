@@ -210,6 +210,10 @@ class Reference:
                                   ctypes.c_int, _u64, ctypes.c_int, _u64]
         lib.bref_deinterleave.argtypes = [ctypes.c_void_p, _u64, ctypes.c_void_p, ctypes.c_int,
                                           _u64, ctypes.c_uint, ctypes.c_int]
+        pd, pi = ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int)
+        lib.bref_chi_square.argtypes = [ctypes.c_void_p, _u64, ctypes.c_int, pd, pi]
+        lib.bref_monobit.argtypes = [ctypes.c_void_p, _u64, pd, pi]
+        lib.bref_serial_correlation.argtypes = [ctypes.c_void_p, _u64, ctypes.c_int, pd, pi]
 
     def modpow2(self, e: int, modulus: int = MODULUS) -> int:
         out = _u64()
@@ -265,6 +269,26 @@ class Reference:
         _check(self.lib.bref_fill(out.ctypes.data, out.size, fmt, n, workers, layout,
                                   seed_index, method, base_offset), "fill")
         return out
+
+    def chi_square(self, x: np.ndarray, bins: int) -> tuple[float, bool]:
+        st, ok = ctypes.c_double(), ctypes.c_int()
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        _check(self.lib.bref_chi_square(x.ctypes.data, x.size, bins, ctypes.byref(st), ctypes.byref(ok)),
+               "chi_square")
+        return st.value, bool(ok.value)
+
+    def monobit(self, z: np.ndarray) -> tuple[float, bool]:
+        st, ok = ctypes.c_double(), ctypes.c_int()
+        z = np.ascontiguousarray(z, dtype=np.uint64)
+        _check(self.lib.bref_monobit(z.ctypes.data, z.size, ctypes.byref(st), ctypes.byref(ok)), "monobit")
+        return st.value, bool(ok.value)
+
+    def serial_correlation(self, x: np.ndarray, lag: int = 1) -> tuple[float, bool]:
+        st, ok = ctypes.c_double(), ctypes.c_int()
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        _check(self.lib.bref_serial_correlation(x.ctypes.data, x.size, lag, ctypes.byref(st),
+                                                ctypes.byref(ok)), "serial_correlation")
+        return st.value, bool(ok.value)
 
     def deinterleave(self, buf: np.ndarray, workers: int, layout: int = INTERLEAVED) -> np.ndarray:
         fmt = FMT_U64 if buf.dtype == np.uint64 else FMT_F64

@@ -14,6 +14,7 @@
 
 #include "bcnrand/generator.hpp"
 #include "bcnrand/parallel.hpp"
+#include "bcnrand/quality.hpp"
 
 namespace {
 
@@ -116,6 +117,32 @@ int bref_deinterleave(const void* in, uint64_t cap, void* out, int fmt, uint64_t
                 std::span<const double>(static_cast<const double*>(in), cap), plan);
             std::memcpy(out, v.data(), v.size() * 8);
         }
+    });
+}
+
+// quality.hpp:27-37 — the reference smoke statistics (for the GPU suite's parity).
+int bref_chi_square(const double* x, uint64_t n, int bins, double* stat, int* pass) {
+    return guarded([&] {
+        const auto r = bcn::quality::chi_square_uniformity(std::span<const double>(x, n), bins);
+        *stat = r.statistic;
+        *pass = r.pass;
+    });
+}
+
+int bref_monobit(const uint64_t* z, uint64_t n, double* stat, int* pass) {
+    return guarded([&] {
+        const auto r = bcn::quality::monobit_mantissa(
+            std::span<const bcn::Residue>(reinterpret_cast<const bcn::Residue*>(z), n));
+        *stat = r.statistic;
+        *pass = r.pass;
+    });
+}
+
+int bref_serial_correlation(const double* x, uint64_t n, int lag, double* rho, int* pass) {
+    return guarded([&] {
+        const auto r = bcn::quality::serial_correlation(std::span<const double>(x, n), lag);
+        *rho = r.statistic;
+        *pass = r.pass;
     });
 }
 

@@ -13,13 +13,14 @@ residues, doubles or floats, computed by sm_100a kernels behind the C ABI in
 from . import device
 from . import generator as gen
 from . import parallel as par
+from . import quality
 from .errors import CudaError, DomainError, InvalidArgument, OutOfRange
 from .generator import (GeneratorState, Method, kInvModulus, kMaxSeedIndex, kMinSeedIndex,
                         kModulus, kPeriod)
 from .parallel import Engine, Format, Layout, PartitionPlan
 
 __all__ = [
-    "gen", "par", "device", "CudaError", "DomainError", "InvalidArgument", "OutOfRange",
+    "gen", "par", "device", "quality", "CudaError", "DomainError", "InvalidArgument", "OutOfRange",
     "GeneratorState", "Method", "Layout", "Format", "Engine", "PartitionPlan",
     "kModulus", "kMinSeedIndex", "kMaxSeedIndex", "kPeriod", "kInvModulus",
 ]

@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <map>
@@ -485,6 +486,34 @@ bcn_status do_fill(void* out, uint64_t capacity, uint64_t n, int fmt, uint32_t w
     return BCN_OK;
 }
 
+// Device view of a caller buffer for the read-only quality kernels: device
+// pointers are used in place, host buffers are copied into a temporary.
+struct DeviceInput {
+    const void* ptr = nullptr;
+    void* owned = nullptr;
+    ~DeviceInput() {
+        if (owned) cudaFree(owned);
+    }
+};
+
+bcn_status stage_input(const void* buf, size_t bytes, int* device, DeviceInput* in, DevCtx** ctx,
+                       cudaStream_t* s, void* stream) {
+    PtrKind kind;
+    bcn_status st = classify(buf, device, &kind);
+    if (st) return st;
+    if (*device < 0) *device = 0;
+    if ((st = get_ctx(*device, ctx))) return st;
+    *s = stream ? static_cast<cudaStream_t>(stream) : (*ctx)->stream;
+    if (kind == PtrKind::Device) {
+        in->ptr = buf;
+        return BCN_OK;
+    }
+    BCN_CUDA(cudaMalloc(&in->owned, bytes));
+    BCN_CUDA(cudaMemcpyAsync(in->owned, buf, bytes, cudaMemcpyHostToDevice, *s));
+    in->ptr = in->owned;
+    return BCN_OK;
+}
+
 }  // namespace
 
 // ===================================================================== C ABI
@@ -807,6 +836,139 @@ bcn_status bcn_fill_constant(void* out, uint64_t nbytes, uint64_t pattern, int d
     }
     if (e != cudaSuccess) return cuda_fail(e, "fill_constant launch");
     if (!stream) BCN_CUDA(cudaStreamSynchronize(s));
+    return BCN_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------ quality suite
+extern "C" {
+
+bcn_status bcn_chi_square_uniformity(const double* samples, uint64_t n, int bins, double* statistic,
+                                     int* dof, int* pass, int device, void* stream) {
+    // quality.cpp:21-54 (same preconditions, same formula on exact counts)
+    if (!statistic || !dof || !pass) return fail(BCN_ERR_INVALID_ARGUMENT, "chi_square: null output");
+    if (n == 0) return fail(BCN_ERR_INVALID_ARGUMENT, "chi_square: no samples");
+    if (bins < 2) return fail(BCN_ERR_INVALID_ARGUMENT, "chi_square: need at least 2 bins");
+    const double expected = static_cast<double>(n) / bins;
+    if (expected < 20.0) return fail(BCN_ERR_INVALID_ARGUMENT, "chi_square: expected count per bin below 20");
+    if (!samples) return fail(BCN_ERR_INVALID_ARGUMENT, "chi_square: null samples");
+    DeviceInput in;
+    DevCtx* c = nullptr;
+    cudaStream_t s;
+    int dev = device;
+    bcn_status st = stage_input(samples, n * sizeof(double), &dev, &in, &c, &s, stream);
+    if (st) return st;
+    unsigned long long* counts = nullptr;
+    BCN_CUDA(cudaMalloc(&counts, static_cast<size_t>(bins) * 8));
+    BCN_CUDA(cudaMemsetAsync(counts, 0, static_cast<size_t>(bins) * 8, s));
+    BCN_CUDA(cudaMemsetAsync(c->flag, 0, sizeof(int), s));
+    const int grid = static_cast<int>(std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(c->sms) * 4));
+    cudaError_t e = launch_chi_hist(static_cast<const double*>(in.ptr), n, bins, counts, c->flag, grid, s);
+    if (e != cudaSuccess) {
+        cudaFree(counts);
+        return cuda_fail(e, "chi_square launch");
+    }
+    std::vector<unsigned long long> h(static_cast<size_t>(bins));
+    int flag = 0;
+    BCN_CUDA(cudaMemcpyAsync(h.data(), counts, h.size() * 8, cudaMemcpyDeviceToHost, s));
+    BCN_CUDA(cudaMemcpyAsync(&flag, c->flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    BCN_CUDA(cudaStreamSynchronize(s));
+    cudaFree(counts);
+    if (flag) return fail(BCN_ERR_INVALID_ARGUMENT, "chi_square: sample outside (0,1)");
+    double stat = 0.0;
+    for (unsigned long long cnt : h) {
+        const double d = static_cast<double>(cnt) - expected;
+        stat += d * d / expected;
+    }
+    *dof = bins - 1;
+    *statistic = stat;
+    *pass = std::fabs(stat - *dof) <= 4.5 * std::sqrt(2.0 * *dof) ? 1 : 0;
+    return BCN_OK;
+}
+
+bcn_status bcn_monobit_mantissa(const uint64_t* residues, uint64_t n, double* statistic, int* worst_bit,
+                                int* pass, int device, void* stream) {
+    // quality.cpp:56-90
+    if (!statistic || !worst_bit || !pass) return fail(BCN_ERR_INVALID_ARGUMENT, "monobit: null output");
+    if (n < 100000) return fail(BCN_ERR_INVALID_ARGUMENT, "monobit: need at least 1e5 residues");
+    if (!residues) return fail(BCN_ERR_INVALID_ARGUMENT, "monobit: null residues");
+    DeviceInput in;
+    DevCtx* c = nullptr;
+    cudaStream_t s;
+    int dev = device;
+    bcn_status st = stage_input(residues, n * 8, &dev, &in, &c, &s, stream);
+    if (st) return st;
+    unsigned long long* ones = nullptr;
+    BCN_CUDA(cudaMalloc(&ones, 53 * 8));
+    BCN_CUDA(cudaMemsetAsync(ones, 0, 53 * 8, s));
+    BCN_CUDA(cudaMemsetAsync(c->flag, 0, sizeof(int), s));
+    const int grid = static_cast<int>(std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(c->sms) * 4));
+    cudaError_t e = launch_monobit(static_cast<const uint64_t*>(in.ptr), n, ones, c->flag, grid, s);
+    if (e != cudaSuccess) {
+        cudaFree(ones);
+        return cuda_fail(e, "monobit launch");
+    }
+    unsigned long long h[53];
+    int flag = 0;
+    BCN_CUDA(cudaMemcpyAsync(h, ones, sizeof(h), cudaMemcpyDeviceToHost, s));
+    BCN_CUDA(cudaMemcpyAsync(&flag, c->flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    BCN_CUDA(cudaStreamSynchronize(s));
+    cudaFree(ones);
+    if (flag) return fail(BCN_ERR_INVALID_ARGUMENT, "monobit: residue out of range");
+    const double nn = static_cast<double>(n);
+    double worst = 0.0;
+    int wb = 5;
+    for (int bit = 5; bit < 53; ++bit) {
+        const double dev_ = std::fabs(static_cast<double>(h[bit]) / nn - 0.5);
+        if (dev_ > worst) {
+            worst = dev_;
+            wb = bit;
+        }
+    }
+    *statistic = worst;
+    *worst_bit = wb;
+    *pass = worst <= 4.5 / (2.0 * std::sqrt(nn)) ? 1 : 0;
+    return BCN_OK;
+}
+
+bcn_status bcn_serial_correlation(const double* samples, uint64_t n, int lag, double* rho, int* pass,
+                                  int device, void* stream) {
+    // quality.cpp:92-118; per-block partial sums, fixed-order host reduction.
+    if (!rho || !pass) return fail(BCN_ERR_INVALID_ARGUMENT, "serial_correlation: null output");
+    if (lag < 1) return fail(BCN_ERR_INVALID_ARGUMENT, "serial_correlation: lag must be positive");
+    if (n < 100000) return fail(BCN_ERR_INVALID_ARGUMENT, "serial_correlation: need at least 1e5 samples");
+    if (!samples) return fail(BCN_ERR_INVALID_ARGUMENT, "serial_correlation: null samples");
+    DeviceInput in;
+    DevCtx* c = nullptr;
+    cudaStream_t s;
+    int dev = device;
+    bcn_status st = stage_input(samples, n * sizeof(double), &dev, &in, &c, &s, stream);
+    if (st) return st;
+    const uint64_t pairs = n - static_cast<uint64_t>(lag);
+    constexpr int kGrid = 592;  // fixed: the reduction order does not depend on the device
+    double* part = nullptr;
+    BCN_CUDA(cudaMalloc(&part, kGrid * 5 * sizeof(double)));
+    cudaError_t e = launch_lag_sums(static_cast<const double*>(in.ptr), pairs, static_cast<uint64_t>(lag), part,
+                                    kGrid, s);
+    if (e != cudaSuccess) {
+        cudaFree(part);
+        return cuda_fail(e, "serial_correlation launch");
+    }
+    std::vector<double> h(kGrid * 5);
+    BCN_CUDA(cudaMemcpyAsync(h.data(), part, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+    BCN_CUDA(cudaStreamSynchronize(s));
+    cudaFree(part);
+    double sum[5] = {0, 0, 0, 0, 0};
+    for (int b = 0; b < kGrid; ++b)
+        for (int k = 0; k < 5; ++k) sum[k] += h[b * 5 + k];
+    const double np = static_cast<double>(pairs);
+    const double vx = sum[2] / np - (sum[0] / np) * (sum[0] / np);
+    const double vy = sum[3] / np - (sum[1] / np) * (sum[1] / np);
+    const double cov = sum[4] / np - (sum[0] / np) * (sum[1] / np);
+    const double r = (vx > 0.0 && vy > 0.0) ? cov / std::sqrt(vx * vy) : std::nan("");
+    *rho = r;
+    *pass = std::isfinite(r) && std::fabs(r) <= 4.5 / std::sqrt(static_cast<double>(n)) ? 1 : 0;
     return BCN_OK;
 }
 

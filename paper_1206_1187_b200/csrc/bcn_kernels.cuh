@@ -134,6 +134,15 @@ cudaError_t launch_digest(const DigestArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_constant(const ConstArgs& a, int grid, int block, cudaStream_t s);
 cudaError_t launch_transpose(const TransposeArgs& a, cudaStream_t s);
 
+// Quality smoke suite (bcn_quality.cu).
+constexpr int kChiSmemBins = 16384;
+cudaError_t launch_chi_hist(const double* u, uint64_t n, int bins, unsigned long long* counts, int* error,
+                            int grid, cudaStream_t s);
+cudaError_t launch_monobit(const uint64_t* z, uint64_t n, unsigned long long* ones, int* error, int grid,
+                           cudaStream_t s);
+cudaError_t launch_lag_sums(const double* x, uint64_t pairs, uint64_t lag, double* out, int grid,
+                            cudaStream_t s);
+
 // Kernels launched through this library so far (process-wide).
 uint64_t launch_count();
 

@@ -52,13 +52,13 @@ def test_cpp_dropin_suite(cuda):
 
 @pytest.mark.gpu
 def test_reference_unit_tests_pass_on_the_b200_library(cuda):
-    """The reference's test_generator.cpp / test_parallel.cpp (23 cases,
+    """The reference's test_generator.cpp / test_parallel.cpp / test_quality.cpp (32 cases,
     ~3.5M assertions incl. worker/layout invariance and base_offset windows)
     pass when compiled against the drop-in headers and run on the GPU."""
     if not os.path.exists(REFTESTS):
         pytest.skip("oracle/_ref/ref_tests_on_b200 not built (needs /root/reference at build time)")
     out = _run(REFTESTS)
-    assert "test cases: 23" in out
+    assert "test cases: 32" in out
 
 
 @pytest.mark.gpu

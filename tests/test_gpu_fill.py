@@ -303,3 +303,37 @@ def test_config2_full_size_digests(bcn, cuda, oracle):
         d = bcn.device.digest(half.view(torch.int64), index_base=h * (n // 2))
         parts = [(parts[0] + d[0]) % (1 << 64), (parts[1] + d[1]) % (1 << 64)]
     assert parts == [whole[0], whole[1]]
+
+
+# ------------------------------------------------------ quality suite (§8f.4)
+def test_quality_suite_matches_reference(bcn, cuda, oracle, reference):
+    """quality.cpp on the GPU: chi-square and monobit statistics bit-identical to
+    the reference on the same data; the lag correlation within 1e-12 (a
+    floating-point sum in a different order); pass flags equal."""
+    n = 10**6
+    u = oracle.fill(n, O.FMT_F64)
+    z = oracle.fill(n, O.FMT_U64)
+    q = bcn.quality
+    for bins in (10, 1000, 20000, 40000):
+        if n / bins < 20:
+            continue
+        r = q.chi_square_uniformity(torch.from_numpy(u).to(cuda), bins)
+        want = reference.chi_square(u, bins)
+        assert (r.statistic, r.passed) == want and r.dof == bins - 1
+    r = q.monobit_mantissa(torch.from_numpy(z.view(np.int64)).to(cuda))
+    assert (r.statistic, r.passed) == reference.monobit(z)
+    for lag in (1, 2, 17):
+        r = q.serial_correlation(u, lag)  # host input
+        rho, ok = reference.serial_correlation(u, lag)
+        assert abs(r.statistic - rho) <= 1e-12 and r.passed == ok
+    # degenerate inputs fail like the reference (test_quality.cpp:52-100)
+    const = np.full(200000, 0.5)
+    assert not q.chi_square_uniformity(const, 1000).passed
+    same = np.full(150000, 123456789012345, dtype=np.uint64)
+    assert not q.monobit_mantissa(same).passed
+    ramp = (np.arange(200000) + 0.5) / 200000
+    assert q.serial_correlation(ramp).statistic > 0.99
+    with pytest.raises(bcn.InvalidArgument):
+        q.chi_square_uniformity(np.full(1000, 0.5), 100)
+    with pytest.raises(bcn.InvalidArgument):
+        q.chi_square_uniformity(np.array([0.5] * 100 + [1.5] * 100000), 10)
