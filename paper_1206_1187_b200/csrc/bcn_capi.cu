@@ -12,10 +12,13 @@
 #include <atomic>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
 #include <string>
+#include <condition_variable>
+#include <functional>
 #include <thread>
 #include <vector>
 
@@ -143,6 +146,17 @@ std::atomic<double> g_pace_gbs{kDefaultPaceGBs};
 std::atomic<int> g_pace_cps{2};
 std::atomic<int> g_pace_formats{(1 << kFmtU64) | (1 << kFmtF64)};
 
+// CTAs of the paced grid: ctas_per_sm x SMs, or BCN_PACE_GRID (an
+// exploration override: total CTAs, e.g. to leave SMs idle under a power cap).
+uint64_t paced_grid(const DevCtx* c) {
+    static const long env = [] {
+        const char* v = std::getenv("BCN_PACE_GRID");
+        return v ? std::strtol(v, nullptr, 10) : 0L;
+    }();
+    if (env > 0) return static_cast<uint64_t>(env);
+    return static_cast<uint64_t>(c->sms) * g_pace_cps.load();
+}
+
 uint64_t pace_gap_q8(int grid, double gbs) {
     // One CTA round writes grid * 8 rows * 1 KiB; 1 GB/s == 1 byte/ns.
     return static_cast<uint64_t>(256.0 * grid * (kPacedThreads / 32 - 1) * 1024.0 / gbs);
@@ -243,14 +257,15 @@ cudaError_t enqueue_affine(const FillJob& j, char* dptr, uint64_t slot0, uint64_
             // Paced path (by default for the 8-byte formats; f32 with the
             // FP64 engine is FP64-pipe bound below the write roof).
             constexpr uint64_t kWorkers = kPacedThreads / 32 - 1;
-            const uint64_t want = static_cast<uint64_t>(j.ctx->sms) * g_pace_cps.load();
+            const uint64_t want = paced_grid(j.ctx);
             const int grid = static_cast<int>(std::max<uint64_t>(1, std::min(want, (rows + kWorkers - 1) / kWorkers)));
-            PacedArgs pa;
+            PacedArgs pa{};
             pa.out = c.out;
             pa.rows = rows;
             pa.e0 = c.e0;
             pa.jump = mult_for_steps(static_cast<__int128>(row) * grid * kWorkers);
             pa.gap_q8 = pace_gap_q8(grid, g_pace_gbs.load());
+            pa.mode = kPacedContiguous;
             e = launch_paced(j.fmt, j.engine, pa, grid, j.stream);
         } else {
             const int grid = grid_for_rows(j.ctx, j.fmt, j.engine, false, rows);
@@ -302,8 +317,33 @@ cudaError_t enqueue_region(const FillJob& j, char* dptr, uint64_t slot0, uint64_
         r.jump_wrap = mult_for_steps((static_cast<__int128>(r.adv_b) - static_cast<__int128>(width)) *
                                          static_cast<__int128>(p.wpw) +
                                      adv_a + 1);
-        const int grid = grid_for_rows(j.ctx, j.fmt, engine, true, rows);
-        e = launch_interleaved(j.fmt, engine, r, grid, kContigThreads, j.stream);
+        if (g_pace_gbs.load() > 0.0 && (g_pace_formats.load() >> j.fmt & 1)) {
+            // Paced, grid-strided: each stream advances nwk rows = S slots per round.
+            constexpr uint64_t kWorkers = kPacedThreads / 32 - 1;
+            const uint64_t want = paced_grid(j.ctx);
+            const int grid = static_cast<int>(std::max<uint64_t>(1, std::min(want, (rows + kWorkers - 1) / kWorkers)));
+            const unsigned __int128 S = static_cast<unsigned __int128>(row) * grid * kWorkers;
+            const uint64_t a_s = static_cast<uint64_t>(S / width), b_s = static_cast<uint64_t>(S % width);
+            PacedArgs pa{};
+            pa.out = r.out;
+            pa.rows = rows;
+            pa.e0 = r.e0;
+            pa.gap_q8 = pace_gap_q8(grid, g_pace_gbs.load());
+            pa.mode = kPacedInterleaved;
+            pa.q0 = r.q0;
+            pa.width = width;
+            pa.i_base = i_base;
+            pa.wpw = p.wpw;
+            pa.adv_b = b_s;
+            pa.jump = mult_for_steps(static_cast<__int128>(b_s) * p.wpw + a_s);
+            pa.jump_wrap = mult_for_steps((static_cast<__int128>(b_s) - static_cast<__int128>(width)) *
+                                              static_cast<__int128>(p.wpw) +
+                                          a_s + 1);
+            e = launch_paced(j.fmt, engine, pa, grid, j.stream);
+        } else {
+            const int grid = grid_for_rows(j.ctx, j.fmt, engine, true, rows);
+            e = launch_interleaved(j.fmt, engine, r, grid, kContigThreads, j.stream);
+        }
         if (e != cudaSuccess) return e;
     }
     const uint64_t done = head + rows * row;
@@ -380,6 +420,81 @@ bcn_status ensure_scratch(DevCtx* c, size_t bytes, bool pinned) {
     return BCN_OK;
 }
 
+// Host copy pool: drains pinned staging buffers into pageable user memory
+// with several threads (one thread reaches ~15 GB/s, well below the D2H rate;
+// first-touch page faults of a fresh buffer are also spread across threads).
+class CopyPool {
+  public:
+    CopyPool() {
+        unsigned hw = std::thread::hardware_concurrency();
+        nthreads_ = hw == 0 ? 4 : std::min(16u, std::max(2u, hw / 2));
+        for (unsigned t = 1; t < nthreads_; ++t) workers_.emplace_back([this, t] { loop(t); });
+    }
+    ~CopyPool() {
+        {
+            std::lock_guard<std::mutex> l(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& w : workers_) w.join();
+    }
+    // memcpy split into nthreads_ slices; returns when all slices are done.
+    void copy(void* dst, const void* src, size_t bytes) {
+        if (bytes < (4u << 20) || nthreads_ == 1) {
+            std::memcpy(dst, src, bytes);
+            return;
+        }
+        std::lock_guard<std::mutex> one_at_a_time(call_mu_);
+        std::unique_lock<std::mutex> l(mu_);
+        dst_ = static_cast<char*>(dst);
+        src_ = static_cast<const char*>(src);
+        bytes_ = bytes;
+        pending_ = nthreads_ - 1;
+        ++gen_;
+        l.unlock();
+        cv_.notify_all();
+        slice(0);
+        l.lock();
+        done_cv_.wait(l, [this] { return pending_ == 0; });
+    }
+
+  private:
+    void slice(unsigned t) {
+        const size_t per = (bytes_ / nthreads_ + 63) & ~size_t{63};
+        const size_t b = std::min(bytes_, per * t), e = std::min(bytes_, b + per);
+        const size_t end = t + 1 == nthreads_ ? bytes_ : e;
+        if (end > b) std::memcpy(dst_ + b, src_ + b, end - b);
+    }
+    void loop(unsigned t) {
+        uint64_t seen = 0;
+        for (;;) {
+            std::unique_lock<std::mutex> l(mu_);
+            cv_.wait(l, [&] { return stop_ || gen_ != seen; });
+            if (stop_) return;
+            seen = gen_;
+            l.unlock();
+            slice(t);
+            l.lock();
+            if (--pending_ == 0) done_cv_.notify_one();
+        }
+    }
+    unsigned nthreads_ = 1;
+    std::vector<std::thread> workers_;
+    std::mutex mu_, call_mu_;
+    std::condition_variable cv_, done_cv_;
+    bool stop_ = false;
+    uint64_t gen_ = 0;
+    unsigned pending_ = 0;
+    char* dst_ = nullptr;
+    const char* src_ = nullptr;
+    size_t bytes_ = 0;
+};
+
+CopyPool& copy_pool() {
+    static CopyPool pool;
+    return pool;
+}
+
 // Host output: generate chunks on the device, D2H on alternating streams.
 bcn_status fill_host(FillJob& j, char* out, bool out_pinned) {
     DevCtx* c = j.ctx;
@@ -404,7 +519,7 @@ bcn_status fill_host(FillJob& j, char* out, bool out_pinned) {
                 const int pb = b ^ 1;
                 const uint64_t q0 = (k - 1) * chunk_items, q1 = std::min(n, q0 + chunk_items);
                 BCN_CUDA(cudaStreamSynchronize(c->copy[pb]));
-                std::memcpy(out + q0 * isz, c->pinned[pb], (q1 - q0) * isz);
+                copy_pool().copy(out + q0 * isz, c->pinned[pb], (q1 - q0) * isz);
             }
         }
     }
@@ -413,7 +528,7 @@ bcn_status fill_host(FillJob& j, char* out, bool out_pinned) {
     if (!out_pinned && nchunks >= 1) {
         const uint64_t k = nchunks - 1;
         const uint64_t q0 = k * chunk_items, q1 = n;
-        std::memcpy(out + q0 * isz, c->pinned[k & 1], (q1 - q0) * isz);
+        copy_pool().copy(out + q0 * isz, c->pinned[k & 1], (q1 - q0) * isz);
     }
     return BCN_OK;
 }
@@ -827,7 +942,12 @@ bcn_status bcn_fill_constant(void* out, uint64_t nbytes, uint64_t pattern, int d
         const uint64_t rows = nbytes / 1024;
         const uint64_t want = static_cast<uint64_t>(c->sms) * g_pace_cps.load();
         const int grid = static_cast<int>(std::max<uint64_t>(1, std::min(want, (rows + kWorkers - 1) / kWorkers)));
-        PacedArgs pa{out, rows, pattern, Mult{}, pace_gap_q8(grid, g_pace_gbs.load())};
+        PacedArgs pa{};
+        pa.out = out;
+        pa.rows = rows;
+        pa.e0 = pattern;
+        pa.gap_q8 = pace_gap_q8(grid, g_pace_gbs.load());
+        pa.mode = kPacedConstant;
         e = launch_paced(kFmtU64, -1, pa, grid, s);
     } else {
         ConstArgs ca{out, nbytes / 1024, pattern, static_cast<uint32_t>(g_row_order.load())};

@@ -247,9 +247,11 @@ __device__ __forceinline__ uint64_t global_ns() {
     return t;
 }
 
-template <int FMT, int ENG, bool CONST>
+template <int FMT, int ENG, int MODE>
 __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a) {
     using E = Eng<ENG>;
+    constexpr bool CONST = MODE == kPacedConstant;
+    constexpr bool INTER = MODE == kPacedInterleaved;
     constexpr int V = Fmt<FMT>::kVec;
     constexpr uint64_t ROW = 32ull * V;
     constexpr int kWorkers = kPacedThreads / 32 - 1;
@@ -280,12 +282,23 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
     const uint64_t w = first + warp;
     const uint64_t count = a.rows > w ? (a.rows - w + nwk - 1) / nwk : 0;
     typename E::State st[V];
+    uint64_t col[INTER ? V : 1];  // interleaved: worker index of each stream's slot
     if (!CONST && count) {
-        uint64_t z = dev_state_from_exp(dev_exp_at(a.e0, w * ROW + lane * V));
+        if constexpr (INTER) {
 #pragma unroll
-        for (int v = 0; v < V; ++v) {
-            st[v] = E::from_canonical(z);
-            if (v + 1 < V) z = step_modified_barrett(z);
+            for (int v = 0; v < V; ++v) {
+                const uint64_t q = a.q0 + w * ROW + lane * V + v;
+                col[v] = q % a.width;
+                const uint64_t j = col[v] * a.wpw + a.i_base + q / a.width;
+                st[v] = E::from_canonical(dev_state_from_exp(dev_exp_at(a.e0, j)));
+            }
+        } else {
+            uint64_t z = dev_state_from_exp(dev_exp_at(a.e0, w * ROW + lane * V));
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                st[v] = E::from_canonical(z);
+                if (v + 1 < V) z = step_modified_barrett(z);
+            }
         }
     }
     constexpr uint64_t kRowBytes = ROW * sizeof(typename Fmt<FMT>::Item);
@@ -294,7 +307,7 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
     const Mult k = a.jump;
     for (uint64_t r = 0; r < rounds; ++r) {
         uint64_t bits[V];
-        if (CONST) {
+        if constexpr (CONST) {
 #pragma unroll
             for (int v = 0; v < V; ++v) bits[v] = a.e0;
         } else {
@@ -303,7 +316,14 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kPacedThreads) : "memory");
         if (r < count) pack_store<FMT>(p, bits);
-        if (!CONST) {
+        if constexpr (INTER) {
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                const bool same = col[v] + a.adv_b < a.width;
+                st[v] = E::mul(st[v], same ? k : a.jump_wrap);
+                col[v] = same ? col[v] + a.adv_b : col[v] + a.adv_b - a.width;
+            }
+        } else if constexpr (!CONST) {
 #pragma unroll
             for (int v = 0; v < V; ++v) st[v] = E::mul(st[v], k);
         }
@@ -635,6 +655,33 @@ __global__ void __launch_bounds__(256) k_transpose(const TransposeArgs a) {
     }
 }
 
+// Narrow regions (width <= 32 workers): a CTA loads kNarrowTile consecutive
+// physical slots (whole rows of the [rows x width] region) with coalesced
+// reads, then writes each worker's run of rows contiguously.
+constexpr int kNarrowTile = 4096;
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_transpose_narrow(const TransposeArgs a) {
+    __shared__ T tile[kNarrowTile];
+    const T* in = static_cast<const T*>(a.in);
+    T* out = static_cast<T*>(a.out);
+    const uint64_t rows_per_tile = kNarrowTile / a.width;
+    for (uint64_t r0 = static_cast<uint64_t>(blockIdx.x) * rows_per_tile; r0 < a.rows;
+         r0 += static_cast<uint64_t>(gridDim.x) * rows_per_tile) {
+        const uint64_t nr = a.rows - r0 < rows_per_tile ? a.rows - r0 : rows_per_tile;
+        const uint64_t cnt = nr * a.width;
+        const T* src = in + a.p0 + r0 * a.width;
+        for (uint64_t k = threadIdx.x; k < cnt; k += blockDim.x) tile[k] = src[k];
+        __syncthreads();
+        const unsigned nr32 = static_cast<unsigned>(nr), width32 = static_cast<unsigned>(a.width);
+        for (unsigned k = threadIdx.x; k < static_cast<unsigned>(cnt); k += blockDim.x) {
+            const unsigned w = k / nr32, i = k - w * nr32;  // 32-bit: cnt <= kNarrowTile
+            out[w * a.wpw + a.i_base + r0 + i] = tile[i * width32 + w];
+        }
+        __syncthreads();
+    }
+}
+
 // ============================================================ launchers
 std::atomic<uint64_t> g_launches{0};
 
@@ -709,17 +756,26 @@ cudaError_t launch_contig(int fmt, int engine, const ContigArgs& a, int grid, in
 }
 
 namespace {
-template <int FMT>
-cudaError_t paced_fmt(int engine, const PacedArgs& a, int grid, cudaStream_t s) {
+template <int FMT, int MODE>
+cudaError_t paced_mode(int engine, const PacedArgs& a, int grid, cudaStream_t s) {
     switch (engine) {
-        case kEngBarrett: k_fill_paced<FMT, kEngBarrett, false><<<grid, kPacedThreads, 0, s>>>(a); break;
-        case kEngMontgomery: k_fill_paced<FMT, kEngMontgomery, false><<<grid, kPacedThreads, 0, s>>>(a); break;
-        case kEngFP64: k_fill_paced<FMT, kEngFP64, false><<<grid, kPacedThreads, 0, s>>>(a); break;
-        case kEngMixed: k_fill_paced<FMT, kEngMixed, false><<<grid, kPacedThreads, 0, s>>>(a); break;
-        case -1: k_fill_paced<FMT, kEngBarrett, true><<<grid, kPacedThreads, 0, s>>>(a); break;
+        case kEngBarrett: k_fill_paced<FMT, kEngBarrett, MODE><<<grid, kPacedThreads, 0, s>>>(a); break;
+        case kEngMontgomery: k_fill_paced<FMT, kEngMontgomery, MODE><<<grid, kPacedThreads, 0, s>>>(a); break;
+        case kEngFP64: k_fill_paced<FMT, kEngFP64, MODE><<<grid, kPacedThreads, 0, s>>>(a); break;
+        case kEngMixed: k_fill_paced<FMT, kEngMixed, MODE><<<grid, kPacedThreads, 0, s>>>(a); break;
         default: return cudaErrorInvalidValue;
     }
     return counted(cudaGetLastError());
+}
+
+template <int FMT>
+cudaError_t paced_fmt(int engine, const PacedArgs& a, int grid, cudaStream_t s) {
+    if (engine == -1) {
+        k_fill_paced<FMT, kEngBarrett, kPacedConstant><<<grid, kPacedThreads, 0, s>>>(a);
+        return counted(cudaGetLastError());
+    }
+    return a.mode == kPacedInterleaved ? paced_mode<FMT, kPacedInterleaved>(engine, a, grid, s)
+                                       : paced_mode<FMT, kPacedContiguous>(engine, a, grid, s);
 }
 }  // namespace
 
@@ -827,6 +883,15 @@ cudaError_t launch_constant(const ConstArgs& a, int grid, int block, cudaStream_
 
 cudaError_t launch_transpose(const TransposeArgs& a, cudaStream_t s) {
     if (a.rows == 0 || a.width == 0) return cudaSuccess;
+    if (a.width <= 32) {
+        const uint64_t tiles = (a.rows + kNarrowTile / a.width - 1) / (kNarrowTile / a.width);
+        const unsigned grid = static_cast<unsigned>(tiles < 148 * 8 ? tiles : 148 * 8);
+        if (a.itemsize == 8)
+            k_transpose_narrow<uint64_t><<<grid, 256, 0, s>>>(a);
+        else
+            k_transpose_narrow<uint32_t><<<grid, 256, 0, s>>>(a);
+        return counted(cudaGetLastError());
+    }
     const dim3 grid(static_cast<unsigned>((a.width + 31) / 32), static_cast<unsigned>((a.rows + 31) / 32));
     if (grid.y > 65535u) return cudaErrorInvalidValue;
     const dim3 block(32, 8);

@@ -35,12 +35,16 @@ struct ContigArgs {
 
 // Paced contiguous fill (k_fill_paced): grid-strided rows metered to a
 // target HBM write rate by one pacer warp per CTA.
+enum PacedMode : int { kPacedContiguous = 0, kPacedConstant = 1, kPacedInterleaved = 2 };
 struct PacedArgs {
     void* out;        // 32-byte aligned
     uint64_t rows;    // rows of 32 lanes x 32 bytes
     uint64_t e0;      // exponent of element 0 (or the 8-byte pattern, Constant)
-    Mult jump;        // 2^(53 * nwk * ROW) mod m, nwk = grid * 8 worker warps
+    Mult jump;        // contiguous: 2^(53 * nwk * ROW); interleaved: the same-row advance
     uint64_t gap_q8;  // ns between CTA rounds, x256 (0 = unpaced)
+    int mode;         // PacedMode (interleaved uses the fields below, as InterleavedArgs)
+    uint64_t q0, width, i_base, wpw, adv_b;
+    Mult jump_wrap;
 };
 
 // Interleaved region fast path (reference Layout::Interleaved,
