@@ -225,10 +225,19 @@ def main() -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # One process per GPU. BCN_DIST_BACKEND=gloo lets several ranks share one
+    # GPU (NCCL refuses duplicate devices) so the multi-rank path can be
+    # exercised on a single-GPU box; collectives then use CPU tensors.
+    backend = os.environ.get("BCN_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    coll_dev = dev if backend == "nccl" else None
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     def barrier():
         if world > 1:
@@ -291,7 +300,7 @@ def main() -> None:
     # Headline: device-resident fill, every step writes this rank's whole share.
     with ClockSampler(local) as clocks:
         per, total_ms, launches = timed(step, args.steps, args.warmup)
-    total_ms = sharding.max_over_ranks(total_ms, dev)
+    total_ms = sharding.max_over_ranks(total_ms, coll_dev)
     value = total_items * args.steps / (total_ms * 1e-3)
     avg_step_ms = statistics.mean(per)
     launches_per_step = max(1, launches // args.steps)
@@ -328,7 +337,7 @@ def main() -> None:
                           stream=stream)
         parts.append(B.device.digest(raw[:c], index_base=b))
     local_digest = sharding.combine(parts)
-    global_digest = sharding.allgather_digest(local_digest, dev) if world > 1 else local_digest
+    global_digest = sharding.allgather_digest(local_digest, coll_dev) if world > 1 else local_digest
     verified = None
     if args.workload == "c5" and args.fmt == "f64":
         try:
@@ -348,7 +357,7 @@ def main() -> None:
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
             B.par.fill_format(host, hplan, A0, B.Method.BarrettModified, start, fmt, engine=engine)
-        dt = sharding.max_over_ranks(time.perf_counter() - t0, dev)
+        dt = sharding.max_over_ranks(time.perf_counter() - t0, coll_dev)
         barrier()
         e2e = {"value": total_items * args.e2e_steps / dt, "unit": UNIT, "h2d_bytes_per_step": 0,
                "d2h_bytes_per_step": count * isz, "steps": args.e2e_steps,

@@ -337,3 +337,31 @@ def test_quality_suite_matches_reference(bcn, cuda, oracle, reference):
         q.chi_square_uniformity(np.full(1000, 0.5), 100)
     with pytest.raises(bcn.InvalidArgument):
         q.chi_square_uniformity(np.array([0.5] * 100 + [1.5] * 100000), 10)
+
+
+# ---------------------------------------------------------- multi-rank bench
+def test_bench_two_ranks_share_one_gpu(bcn, cuda):
+    """bench.py under torchrun with 2 ranks (gloo, both on cuda:0): shards,
+    max-over-ranks timing and the digest all-gather run end to end, and the C5
+    strong-scaling digest over 2 ranks equals the committed 2^36 digest."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, BCN_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29531", os.path.join(root, "bench.py"),
+           "--gpus", "2", "--steps", "3", "--warmup", "3", "--no-e2e", "--no-cpu", "--log2n", "26"]
+    r = subprocess.run(cmd, capture_output=True, text=True, env=env, cwd=root, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["gpu_launches"] >= 3
+    # The 2-rank digest of 2^27 logical items equals a single fill of 2^27.
+    import oracle as O
+
+    n = 1 << 27
+    buf = torch.empty(n, dtype=torch.float64, device=cuda)
+    bcn.par.fill(buf, bcn.par.make_plan(n, 1), O.MIN_SEED, sync=True)
+    assert [str(x) for x in bcn.device.digest(buf.view(torch.int64))] == line["digest"]
