@@ -168,9 +168,15 @@ __device__ __forceinline__ MixedState mul_mixed(MixedState x, double com, int64_
     return MixedState{rs, __ll2double_rn(rs)};
 }
 
-// Canonical residue (as an exact double) of a balanced FP64 state.
+// Canonical residue (as an exact double) of a balanced FP64 state: add m when
+// the sign bit is set. The addend is built with integer ops on the high word
+// (SHF + 2 LOP3) instead of a DSETP + 2 FSEL, keeping the FP64 pipe for the
+// arithmetic (s is never -0: it is a nonzero unit).
 __device__ __forceinline__ double fp64_canonical(double s) {
-    return __dadd_rn(s, s < 0.0 ? kModulusD : 0.0);
+    const int hi = __double2hiint(s);
+    const int mask = hi >> 31;  // all ones iff s < 0
+    const double add = __hiloint2double(mask & __double2hiint(kModulusD), mask & __double2loint(kModulusD));
+    return __dadd_rn(s, add);
 }
 
 // reference generator.hpp:74-78: double(z) * kInvModulus with one RN multiply.
