@@ -854,7 +854,9 @@ bcn_status bcn_deinterleave(const void* in, void* out, uint64_t n, uint32_t work
         const uint64_t p0 = region == 0 ? 0 : sc * p.workers;
         const uint64_t ib = region == 0 ? 0 : sc;
         if (rows == 0 || width == 0) continue;
-        const uint64_t max_rows = 65535ull * 32;
+        // The wide kernel's 2D grid caps a launch at 65535*32 rows; the narrow
+        // kernel (width <= 32) is grid-strided and takes the region whole.
+        const uint64_t max_rows = width <= 32 ? rows : 65535ull * 32;
         for (uint64_t r0 = 0; r0 < rows; r0 += max_rows) {
             t.p0 = p0 + r0 * width;
             t.rows = std::min(max_rows, rows - r0);
