@@ -48,42 +48,40 @@ __global__ void __launch_bounds__(256) k_chi_hist(const double* u, uint64_t n, i
 
 // One counts of bits 5..52 of w = floor(z 2^53 / m) (quality.cpp:66-73).
 // w is the modified-Barrett quotient q3, +1 when the step needed its
-// correction; residues >= m raise the error flag. Counting is warp-wide: one
-// ballot + popc per bit per 32 residues, lane b keeping bit (5+b)'s count and
-// lanes 0..15 also bit (37+b)'s.
+// correction; residues >= m raise the error flag.
 __global__ void __launch_bounds__(256) k_monobit(const uint64_t* z, uint64_t n,
                                                  unsigned long long* ones, int* error) {
-    const unsigned lane = threadIdx.x & 31;
-    unsigned long long c_lo = 0, c_hi = 0;  // bits 5+lane and 37+lane (lane < 16)
+    __shared__ unsigned long long acc[53];
+    for (int b = threadIdx.x; b < 53; b += blockDim.x) acc[b] = 0;
+    __syncthreads();
+    unsigned int local[48];
+#pragma unroll
+    for (int b = 0; b < 48; ++b) local[b] = 0;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    const uint64_t n_round = (n + 31) & ~uint64_t{31};
-    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n_round; i += stride) {
-        uint64_t w = 0;
-        if (i < n) {
-            const uint64_t v = z[i];
-            if (v >= kModulus) {
-                *error = 1;
-            } else if (v != 0) {
-                const uint64_t hi = __umul64hi(v, kMu), lo = v * kMu;
-                w = (hi << 11) | (lo >> 53);  // q3 in {Q-1, Q}
-                const uint64_t r = 0x20000000000000ull - ((w * kModulus) & 0x1FFFFFFFFFFFFFull);
-                if (r >= kModulus) ++w;       // the step's correction => q3 was Q-1
-            }
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint64_t v = z[i];
+        if (v >= kModulus) {
+            *error = 1;
+            continue;
         }
-        const unsigned lo32 = static_cast<unsigned>(w >> 5), hi32 = static_cast<unsigned>(w >> 37);
+        const uint64_t hi = __umul64hi(v, kMu), lo = v * kMu;
+        uint64_t w = (hi << 11) | (lo >> 53);  // q3 in {Q-1, Q}
+        const uint64_t r = 0x20000000000000ull - ((w * kModulus) & 0x1FFFFFFFFFFFFFull);
+        if (v != 0 && r >= kModulus) ++w;      // the step's correction => q3 was Q-1
+        if (v == 0) w = 0;
 #pragma unroll
-        for (int b = 0; b < 32; ++b) {
-            const unsigned cnt = __popc(__ballot_sync(0xffffffffu, (lo32 >> b) & 1));
-            if (lane == b) c_lo += cnt;
-        }
-#pragma unroll
-        for (int b = 0; b < 16; ++b) {
-            const unsigned cnt = __popc(__ballot_sync(0xffffffffu, (hi32 >> b) & 1));
-            if (lane == b) c_hi += cnt;
-        }
+        for (int b = 0; b < 48; ++b) local[b] += static_cast<unsigned int>((w >> (b + 5)) & 1);
     }
-    if (c_lo) atomicAdd(&ones[5 + lane], c_lo);
-    if (lane < 16 && c_hi) atomicAdd(&ones[37 + lane], c_hi);
+#pragma unroll
+    for (int b = 0; b < 48; ++b) {
+        unsigned int c = local[b];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if ((threadIdx.x & 31) == 0 && c) atomicAdd(&acc[b + 5], static_cast<unsigned long long>(c));
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < 53; b += blockDim.x)
+        if (acc[b]) atomicAdd(&ones[b], acc[b]);
 }
 
 // Per-block partial sums sx, sy, sxx, syy, sxy over pairs (s[i], s[i+lag]),
