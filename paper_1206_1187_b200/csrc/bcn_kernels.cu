@@ -885,7 +885,11 @@ cudaError_t launch_transpose(const TransposeArgs& a, cudaStream_t s) {
     if (a.rows == 0 || a.width == 0) return cudaSuccess;
     if (a.width <= 32) {
         const uint64_t tiles = (a.rows + kNarrowTile / a.width - 1) / (kNarrowTile / a.width);
-        const unsigned grid = static_cast<unsigned>(tiles < 148 * 8 ? tiles : 148 * 8);
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const uint64_t cap = static_cast<uint64_t>(sms) * 8;
+        const unsigned grid = static_cast<unsigned>(tiles < cap ? tiles : cap);
         if (a.itemsize == 8)
             k_transpose_narrow<uint64_t><<<grid, 256, 0, s>>>(a);
         else
