@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <algorithm>
 #include <atomic>
 #include <mutex>
 
@@ -655,28 +656,34 @@ __global__ void __launch_bounds__(256) k_transpose(const TransposeArgs a) {
     }
 }
 
-// Narrow regions (width <= 32 workers): a CTA loads kNarrowTile consecutive
-// physical slots (whole rows of the [rows x width] region) with coalesced
-// reads, then writes each worker's run of rows contiguously.
+// Narrow regions (width <= 32 workers): a CTA takes R consecutive rows of the
+// [rows x width] region (R*width <= kNarrowTile slots, read as one contiguous
+// span: thread t reads row t's `width` items, so a warp covers 32*width
+// consecutive items and every sector it touches is fully used), transposes them
+// into shared memory as [width][R] with an odd pitch (conflict-free), and
+// writes each worker's R consecutive logical items with coalesced stores.
 constexpr int kNarrowTile = 4096;
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_transpose_narrow(const TransposeArgs a) {
-    __shared__ T tile[kNarrowTile];
+    __shared__ T tile[kNarrowTile + 32];
     const T* in = static_cast<const T*>(a.in);
     T* out = static_cast<T*>(a.out);
-    const uint64_t rows_per_tile = kNarrowTile / a.width;
-    for (uint64_t r0 = static_cast<uint64_t>(blockIdx.x) * rows_per_tile; r0 < a.rows;
-         r0 += static_cast<uint64_t>(gridDim.x) * rows_per_tile) {
-        const uint64_t nr = a.rows - r0 < rows_per_tile ? a.rows - r0 : rows_per_tile;
-        const uint64_t cnt = nr * a.width;
-        const T* src = in + a.p0 + r0 * a.width;
-        for (uint64_t k = threadIdx.x; k < cnt; k += blockDim.x) tile[k] = src[k];
+    const unsigned width = static_cast<unsigned>(a.width);
+    unsigned R = kNarrowTile / width;
+    R = R > 256 ? 256 : R;           // one row per thread
+    const unsigned pitch = R | 1;    // odd pitch: w-major writes hit distinct banks
+    for (uint64_t r0 = static_cast<uint64_t>(blockIdx.x) * R; r0 < a.rows;
+         r0 += static_cast<uint64_t>(gridDim.x) * R) {
+        const unsigned nr = static_cast<unsigned>(a.rows - r0 < R ? a.rows - r0 : R);
+        if (threadIdx.x < nr) {
+            const T* src = in + a.p0 + (r0 + threadIdx.x) * width;
+            for (unsigned w = 0; w < width; ++w) tile[w * pitch + threadIdx.x] = src[w];
+        }
         __syncthreads();
-        const unsigned nr32 = static_cast<unsigned>(nr), width32 = static_cast<unsigned>(a.width);
-        for (unsigned k = threadIdx.x; k < static_cast<unsigned>(cnt); k += blockDim.x) {
-            const unsigned w = k / nr32, i = k - w * nr32;  // 32-bit: cnt <= kNarrowTile
-            out[w * a.wpw + a.i_base + r0 + i] = tile[i * width32 + w];
+        for (unsigned w = 0; w < width; ++w) {
+            T* dst = out + w * a.wpw + a.i_base + r0;
+            for (unsigned i = threadIdx.x; i < nr; i += blockDim.x) dst[i] = tile[w * pitch + i];
         }
         __syncthreads();
     }
@@ -884,7 +891,8 @@ cudaError_t launch_constant(const ConstArgs& a, int grid, int block, cudaStream_
 cudaError_t launch_transpose(const TransposeArgs& a, cudaStream_t s) {
     if (a.rows == 0 || a.width == 0) return cudaSuccess;
     if (a.width <= 32) {
-        const uint64_t tiles = (a.rows + kNarrowTile / a.width - 1) / (kNarrowTile / a.width);
+        const uint64_t per = std::min<uint64_t>(256, kNarrowTile / a.width);
+        const uint64_t tiles = (a.rows + per - 1) / per;
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
