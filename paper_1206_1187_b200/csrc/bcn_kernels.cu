@@ -565,24 +565,45 @@ __global__ void __launch_bounds__(kContigThreads) k_fill_bulk(const ContigArgs a
 // SeedArgs.steps == 0: out[t] = state_at(a[t], k[t]) (generator.cpp:42-49).
 // steps > 0: out[t*steps + s] = the (s+1)-th next() from that state.
 __global__ void __launch_bounds__(256) k_seed(const SeedArgs a) {
-    const uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (t >= a.count) return;
-    const uint64_t idx = a.a[t];
-    if (idx < kMinSeed || idx > kMaxSeed) {
-        *a.error = 1;
-        return;
+    // Walk outputs are staged 8 steps at a time in shared memory ([thread][8],
+    // padded) so the block writes each thread's 64-byte pieces with 8 lanes
+    // per piece instead of one 8-byte store per lane per step.
+    constexpr int kChunk = 8;
+    __shared__ uint64_t stage[256][kChunk + 1];
+    const uint64_t t0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x;
+    const uint64_t t = t0 + threadIdx.x;
+    bool live = t < a.count;
+    uint64_t z = 0;
+    if (live) {
+        const uint64_t idx = a.a[t];
+        if (idx < kMinSeed || idx > kMaxSeed) {
+            *a.error = 1;
+            live = false;
+        } else {
+            const uint64_t ae = (idx - kModulus - 1) % kPeriod;
+            const uint64_t e = (ae + (53ull * (a.k[t] % kPeriod)) % kPeriod) % kPeriod;
+            z = dev_state_from_exp(e);
+        }
     }
-    const uint64_t ae = (idx - kModulus - 1) % kPeriod;
-    const uint64_t e = (ae + (53ull * (a.k[t] % kPeriod)) % kPeriod) % kPeriod;
-    uint64_t z = dev_state_from_exp(e);
     if (a.steps == 0) {
-        a.out[t] = z;
+        if (live) a.out[t] = z;
         return;
     }
-    uint64_t* o = a.out + t * a.steps;
-    for (uint32_t s = 0; s < a.steps; ++s) {
-        z = step_modified_barrett(z);
-        o[s] = z;
+    const uint64_t nthreads = a.count - t0 < blockDim.x ? a.count - t0 : blockDim.x;
+    for (uint32_t s0 = 0; s0 < a.steps; s0 += kChunk) {
+        const uint32_t len = a.steps - s0 < kChunk ? a.steps - s0 : kChunk;
+        for (uint32_t s = 0; s < len; ++s) {
+            if (live) z = step_modified_barrett(z);
+            stage[threadIdx.x][s] = z;
+        }
+        __syncthreads();
+        for (uint32_t e = threadIdx.x; e < nthreads * len; e += blockDim.x) {
+            const uint32_t th = e / len, s = e - th * len;
+            const uint64_t src = a.a[t0 + th];
+            if (src >= kMinSeed && src <= kMaxSeed)
+                a.out[(t0 + th) * a.steps + s0 + s] = stage[th][s];
+        }
+        __syncthreads();
     }
 }
 
