@@ -181,6 +181,12 @@ bcn_status bcn_monobit_mantissa(const uint64_t* residues, uint64_t n, double* st
 bcn_status bcn_serial_correlation(const double* samples, uint64_t n, int lag, double* rho, int* pass,
                                   int device, void* stream);
 
+/* cli.cpp:127-131 — the `gen --format text` rendering: one "%.17g\n" line per
+ * value (host, multi-threaded). *written = bytes needed; capacity too small is
+ * BCN_ERR_INVALID_ARGUMENT (24 bytes per value always suffice). */
+bcn_status bcn_format_text(const double* values, uint64_t n, char* out, uint64_t capacity,
+                           uint64_t* written);
+
 #ifdef __cplusplus
 }
 #endif

@@ -47,6 +47,7 @@ SIGNATURES = [
     ("bcn_seed_states", _int, [_vp, _vp, _vp, _u64, _u32, _int, _vp]),
     ("bcn_digest", _int, [_vp, _u64, _u32, _u64, _pu64, _int, _vp]),
     ("bcn_fill_constant", _int, [_vp, _u64, _u64, _int, _vp]),
+    ("bcn_format_text", _int, [_vp, _u64, _vp, _u64, _pu64]),
     ("bcn_chi_square_uniformity", _int, [_vp, _u64, _int, ctypes.POINTER(ctypes.c_double),
                                          ctypes.POINTER(_int), ctypes.POINTER(_int), _int, _vp]),
     ("bcn_monobit_mantissa", _int, [_vp, _u64, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_int),

@@ -1095,3 +1095,37 @@ bcn_status bcn_serial_correlation(const double* samples, uint64_t n, int lag, do
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------ text format
+extern "C" bcn_status bcn_format_text(const double* values, uint64_t n, char* out, uint64_t capacity,
+                                      uint64_t* written) {
+    // cli.cpp:127-131: one "%.17g\n" line per value. Formatted in parallel
+    // slices into per-slice buffers, then concatenated in order.
+    if ((!values && n) || !written || (!out && capacity)) return fail(BCN_ERR_INVALID_ARGUMENT, "format_text: null buffer");
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const uint64_t slices = std::min<uint64_t>(std::max<uint64_t>(1, n / 65536), hw);
+    std::vector<std::string> parts(slices);
+    std::vector<std::thread> pool;
+    auto body = [&](uint64_t k) {
+        const uint64_t b = n * k / slices, e = n * (k + 1) / slices;
+        std::string& o = parts[k];
+        o.reserve((e - b) * 24);
+        char line[64];
+        for (uint64_t i = b; i < e; ++i) {
+            const int len = std::snprintf(line, sizeof(line), "%.17g\n", values[i]);
+            o.append(line, static_cast<size_t>(len));
+        }
+    };
+    for (uint64_t k = 1; k < slices; ++k) pool.emplace_back(body, k);
+    body(0);
+    for (auto& t : pool) t.join();
+    uint64_t total = 0;
+    for (const auto& p : parts) total += p.size();
+    *written = total;
+    if (total > capacity) return fail(BCN_ERR_INVALID_ARGUMENT, "format_text: output buffer too small");
+    for (const auto& p : parts) {
+        std::memcpy(out, p.data(), p.size());
+        out += p.size();
+    }
+    return BCN_OK;
+}
