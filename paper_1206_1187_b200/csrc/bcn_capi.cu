@@ -157,9 +157,11 @@ uint64_t paced_grid(const DevCtx* c) {
     return static_cast<uint64_t>(c->sms) * g_pace_cps.load();
 }
 
-uint64_t pace_gap_q8(int grid, double gbs) {
-    // One CTA round writes grid * 8 rows * 1 KiB; 1 GB/s == 1 byte/ns.
-    return static_cast<uint64_t>(256.0 * grid * (kPacedThreads / 32 - 1) * 1024.0 / gbs);
+uint64_t pace_gap_q8(int grid, double gbs, int fmt) {
+    // One round of the grid writes grid * 8 workers * H rows * 1 KiB;
+    // 1 GB/s == 1 byte/ns.
+    return static_cast<uint64_t>(256.0 * grid * (kPacedThreads / 32 - 1) * paced_rows_per_round(fmt) * 1024.0 /
+                                 gbs);
 }
 
 int grid_for_rows(DevCtx* c, int fmt, int engine, bool interleaved, uint64_t rows) {
@@ -263,8 +265,8 @@ cudaError_t enqueue_affine(const FillJob& j, char* dptr, uint64_t slot0, uint64_
             pa.out = c.out;
             pa.rows = rows;
             pa.e0 = c.e0;
-            pa.jump = mult_for_steps(static_cast<__int128>(row) * grid * kWorkers);
-            pa.gap_q8 = pace_gap_q8(grid, g_pace_gbs.load());
+            pa.jump = mult_for_steps(static_cast<__int128>(row) * grid * kWorkers * paced_rows_per_round(j.fmt));
+            pa.gap_q8 = pace_gap_q8(grid, g_pace_gbs.load(), j.fmt);
             pa.mode = kPacedContiguous;
             e = launch_paced(j.fmt, j.engine, pa, grid, j.stream);
         } else {
@@ -322,13 +324,14 @@ cudaError_t enqueue_region(const FillJob& j, char* dptr, uint64_t slot0, uint64_
             constexpr uint64_t kWorkers = kPacedThreads / 32 - 1;
             const uint64_t want = paced_grid(j.ctx);
             const int grid = static_cast<int>(std::max<uint64_t>(1, std::min(want, (rows + kWorkers - 1) / kWorkers)));
-            const unsigned __int128 S = static_cast<unsigned __int128>(row) * grid * kWorkers;
+            const unsigned __int128 S =
+                static_cast<unsigned __int128>(row) * grid * kWorkers * paced_rows_per_round(j.fmt);
             const uint64_t a_s = static_cast<uint64_t>(S / width), b_s = static_cast<uint64_t>(S % width);
             PacedArgs pa{};
             pa.out = r.out;
             pa.rows = rows;
             pa.e0 = r.e0;
-            pa.gap_q8 = pace_gap_q8(grid, g_pace_gbs.load());
+            pa.gap_q8 = pace_gap_q8(grid, g_pace_gbs.load(), j.fmt);
             pa.mode = kPacedInterleaved;
             pa.q0 = r.q0;
             pa.width = width;
@@ -948,7 +951,7 @@ bcn_status bcn_fill_constant(void* out, uint64_t nbytes, uint64_t pattern, int d
         pa.out = out;
         pa.rows = rows;
         pa.e0 = pattern;
-        pa.gap_q8 = pace_gap_q8(grid, g_pace_gbs.load());
+        pa.gap_q8 = pace_gap_q8(grid, g_pace_gbs.load(), kFmtU64);
         pa.mode = kPacedConstant;
         e = launch_paced(kFmtU64, -1, pa, grid, s);
     } else {

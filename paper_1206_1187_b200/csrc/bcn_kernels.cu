@@ -254,18 +254,22 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
     constexpr bool CONST = MODE == kPacedConstant;
     constexpr bool INTER = MODE == kPacedInterleaved;
     constexpr int V = Fmt<FMT>::kVec;
+    constexpr int H = paced_rows_per_round(FMT);  // rows per worker per round
     constexpr uint64_t ROW = 32ull * V;
     constexpr int kWorkers = kPacedThreads / 32 - 1;
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t nwk = static_cast<uint64_t>(gridDim.x) * kWorkers;
     const uint64_t first = static_cast<uint64_t>(blockIdx.x) * kWorkers;
-    const uint64_t rounds = a.rows > first ? (a.rows - first + nwk - 1) / nwk : 0;
+    // Worker w writes rows w + (H*k + h)*nwk, h < H; a round covers H*nwk rows.
+    const uint64_t per_round = H * nwk;
+    const uint32_t rounds =
+        a.rows > first ? static_cast<uint32_t>((a.rows - first + per_round - 1) / per_round) : 0;
     if (rounds == 0) return;  // uniform across the CTA
     if (warp == kWorkers) {
         // Pacer: release round k no earlier than t0 + k * gap.
         uint64_t t0 = 0;
         if (lane == 0) t0 = global_ns();
-        for (uint64_t k = 0; k < rounds; ++k) {
+        for (uint32_t k = 0; k < rounds; ++k) {
             if (lane == 0 && a.gap_q8) {
                 const uint64_t target = t0 + ((k * a.gap_q8) >> 8);
                 uint64_t now = global_ns();
@@ -281,54 +285,73 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
         return;
     }
     const uint64_t w = first + warp;
-    const uint64_t count = a.rows > w ? (a.rows - w + nwk - 1) / nwk : 0;
-    typename E::State st[V];
-    uint64_t col[INTER ? V : 1];  // interleaved: worker index of each stream's slot
-    if (!CONST && count) {
-        if constexpr (INTER) {
+    // rows this worker owns: w, w+nwk, ... (< a.rows)
+    const uint32_t count = a.rows > w ? static_cast<uint32_t>((a.rows - w + nwk - 1) / nwk) : 0;
+    typename E::State st[H][V];
+    uint64_t col[INTER ? H : 1][INTER ? V : 1];  // interleaved: worker index of each stream's slot
+    if (!CONST) {
 #pragma unroll
-            for (int v = 0; v < V; ++v) {
-                const uint64_t q = a.q0 + w * ROW + lane * V + v;
-                col[v] = q % a.width;
-                const uint64_t j = col[v] * a.wpw + a.i_base + q / a.width;
-                st[v] = E::from_canonical(dev_state_from_exp(dev_exp_at(a.e0, j)));
-            }
-        } else {
-            uint64_t z = dev_state_from_exp(dev_exp_at(a.e0, w * ROW + lane * V));
+        for (int h = 0; h < H; ++h) {
+            const uint64_t row = w + h * nwk;
+            if constexpr (INTER) {
 #pragma unroll
-            for (int v = 0; v < V; ++v) {
-                st[v] = E::from_canonical(z);
-                if (v + 1 < V) z = step_modified_barrett(z);
+                for (int v = 0; v < V; ++v) {
+                    const uint64_t q = a.q0 + row * ROW + lane * V + v;
+                    col[h][v] = q % a.width;
+                    const uint64_t j = col[h][v] * a.wpw + a.i_base + q / a.width;
+                    st[h][v] = E::from_canonical(dev_state_from_exp(dev_exp_at(a.e0, j)));
+                }
+            } else {
+                uint64_t z = dev_state_from_exp(dev_exp_at(a.e0, row * ROW + lane * V));
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    st[h][v] = E::from_canonical(z);
+                    if (v + 1 < V) z = step_modified_barrett(z);
+                }
             }
         }
     }
     constexpr uint64_t kRowBytes = ROW * sizeof(typename Fmt<FMT>::Item);
     char* p = static_cast<char*>(a.out) + w * kRowBytes + lane * 32;
-    const uint64_t pstep = nwk * kRowBytes;
+    const uint64_t hstep = nwk * kRowBytes;
     const Mult k = a.jump;
-    for (uint64_t r = 0; r < rounds; ++r) {
-        uint64_t bits[V];
-        if constexpr (CONST) {
+    uint32_t r = 0;  // this worker's rows done
+    for (uint32_t rd = 0; rd < rounds; ++rd, r += H) {
+        uint64_t bits[H][V];
 #pragma unroll
-            for (int v = 0; v < V; ++v) bits[v] = a.e0;
-        } else {
-#pragma unroll
-            for (int v = 0; v < V; ++v) bits[v] = emit_bits<FMT, E>(st[v]);
-        }
-        asm volatile("bar.sync 1, %0;" ::"n"(kPacedThreads) : "memory");
-        if (r < count) pack_store<FMT>(p, bits);
-        if constexpr (INTER) {
+        for (int h = 0; h < H; ++h)
 #pragma unroll
             for (int v = 0; v < V; ++v) {
-                const bool same = col[v] + a.adv_b < a.width;
-                st[v] = E::mul(st[v], same ? k : a.jump_wrap);
-                col[v] = same ? col[v] + a.adv_b : col[v] + a.adv_b - a.width;
+                if constexpr (CONST)
+                    bits[h][v] = a.e0;
+                else
+                    bits[h][v] = emit_bits<FMT, E>(st[h][v]);
             }
+        asm volatile("bar.sync 1, %0;" ::"n"(kPacedThreads) : "memory");
+        if (r + H <= count) {
+#pragma unroll
+            for (int h = 0; h < H; ++h) pack_store<FMT>(p + h * hstep, bits[h]);
+        } else {
+#pragma unroll
+            for (int h = 0; h < H; ++h)
+                if (r + h < count) pack_store<FMT>(p + h * hstep, bits[h]);
+        }
+        if constexpr (INTER) {
+#pragma unroll
+            for (int h = 0; h < H; ++h)
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    const bool same = col[h][v] + a.adv_b < a.width;
+                    st[h][v] = E::mul(st[h][v], same ? k : a.jump_wrap);
+                    col[h][v] = same ? col[h][v] + a.adv_b : col[h][v] + a.adv_b - a.width;
+                }
         } else if constexpr (!CONST) {
 #pragma unroll
-            for (int v = 0; v < V; ++v) st[v] = E::mul(st[v], k);
+            for (int h = 0; h < H; ++h)
+#pragma unroll
+                for (int v = 0; v < V; ++v) st[h][v] = E::mul(st[h][v], k);
         }
-        p += pstep;
+        p += H * hstep;
     }
 }
 

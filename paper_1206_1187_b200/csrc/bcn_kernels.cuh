@@ -40,7 +40,7 @@ struct PacedArgs {
     void* out;        // 32-byte aligned
     uint64_t rows;    // rows of 32 lanes x 32 bytes
     uint64_t e0;      // exponent of element 0 (or the 8-byte pattern, Constant)
-    Mult jump;        // contiguous: 2^(53 * nwk * ROW); interleaved: the same-row advance
+    Mult jump;        // per round: contiguous 2^(53 * H * nwk * ROW); interleaved: same-row advance
     uint64_t gap_q8;  // ns between CTA rounds, x256 (0 = unpaced)
     int mode;         // PacedMode (interleaved uses the fields below, as InterleavedArgs)
     uint64_t q0, width, i_base, wpw, adv_b;
@@ -162,6 +162,9 @@ constexpr int kStagedL = 15;          // odd: conflict-free strided smem stores
 constexpr int kStagedThreads = 256;
 constexpr int kContigThreads = 256;
 constexpr int kPacedThreads = 288;  // 8 worker warps + 1 pacer warp
+// Rows each paced worker stores per pacer round: 2 for the 8-byte formats (8
+// independent streams per lane), 1 for f32 (already 8 streams per lane).
+__host__ __device__ constexpr int paced_rows_per_round(int fmt) { return fmt == kFmtF32 ? 1 : 2; }
 // Measured default pacing target for the 8-byte formats (DESIGN.md §5,
 // profiles/r01/tune_pace.jsonl): FP64 engine f64/u64 reach ~7.08 TB/s at
 // 7200 vs ~6.25 unpaced; above ~7.3 the write path starts to oversubscribe.
