@@ -157,11 +157,11 @@ uint64_t paced_grid(const DevCtx* c) {
     return static_cast<uint64_t>(c->sms) * g_pace_cps.load();
 }
 
-uint64_t pace_gap_q8(int grid, double gbs, int fmt) {
+uint64_t pace_gap_q8(int grid, double gbs, int fmt, bool constant = false) {
     // One round of the grid writes grid * 8 workers * H rows * 1 KiB;
     // 1 GB/s == 1 byte/ns.
-    return static_cast<uint64_t>(256.0 * grid * (kPacedThreads / 32 - 1) * paced_rows_per_round(fmt) * 1024.0 /
-                                 gbs);
+    return static_cast<uint64_t>(256.0 * grid * (kPacedThreads / 32 - 1) * paced_rows_per_round(fmt, constant) *
+                                 1024.0 / gbs);
 }
 
 int grid_for_rows(DevCtx* c, int fmt, int engine, bool interleaved, uint64_t rows) {
@@ -951,7 +951,7 @@ bcn_status bcn_fill_constant(void* out, uint64_t nbytes, uint64_t pattern, int d
         pa.out = out;
         pa.rows = rows;
         pa.e0 = pattern;
-        pa.gap_q8 = pace_gap_q8(grid, g_pace_gbs.load(), kFmtU64);
+        pa.gap_q8 = pace_gap_q8(grid, g_pace_gbs.load(), kFmtU64, true);
         pa.mode = kPacedConstant;
         e = launch_paced(kFmtU64, -1, pa, grid, s);
     } else {

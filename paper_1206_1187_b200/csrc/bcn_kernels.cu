@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
     constexpr bool CONST = MODE == kPacedConstant;
     constexpr bool INTER = MODE == kPacedInterleaved;
     constexpr int V = Fmt<FMT>::kVec;
-    constexpr int H = paced_rows_per_round(FMT);  // rows per worker per round
+    constexpr int H = paced_rows_per_round(FMT, CONST);  // rows per worker per round
     constexpr uint64_t ROW = 32ull * V;
     constexpr int kWorkers = kPacedThreads / 32 - 1;
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

@@ -162,9 +162,13 @@ constexpr int kStagedL = 15;          // odd: conflict-free strided smem stores
 constexpr int kStagedThreads = 256;
 constexpr int kContigThreads = 256;
 constexpr int kPacedThreads = 288;  // 8 worker warps + 1 pacer warp
-// Rows each paced worker stores per pacer round: 2 for the 8-byte formats (8
-// independent streams per lane), 1 for f32 (already 8 streams per lane).
-__host__ __device__ constexpr int paced_rows_per_round(int fmt) { return fmt == kFmtF32 ? 1 : 2; }
+// Rows each paced worker stores per pacer round: 2 for the generating kernels
+// of the 8-byte formats (8 independent streams per lane), 1 for f32 (already 8
+// streams per lane) and for the Constant writer (no compute spreads its
+// stores, and a 2-row burst per round measurably lowers HBM efficiency).
+__host__ __device__ constexpr int paced_rows_per_round(int fmt, bool constant = false) {
+    return (constant || fmt == kFmtF32) ? 1 : 2;
+}
 // Measured default pacing target for the 8-byte formats (DESIGN.md §5,
 // profiles/r01/tune_pace.jsonl): FP64 engine f64/u64 reach ~7.08 TB/s at
 // 7200 vs ~6.25 unpaced; above ~7.3 the write path starts to oversubscribe.
