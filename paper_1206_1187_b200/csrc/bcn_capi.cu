@@ -11,18 +11,18 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <condition_variable>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <string>
-#include <condition_variable>
-#include <functional>
 #include <thread>
 #include <vector>
 
-#include "../../include/bcnrand_b200.h"
+#include "bcnrand_b200.h"
 #include "bcn_kernels.cuh"
 
 using namespace bcn_b200;
@@ -89,7 +89,9 @@ struct DevCtx {
     unsigned long long* digest = nullptr;
     int* flag = nullptr;
     std::map<int, int> occ;           // (fmt*8+engine) -> blocks per SM
+    std::mutex occ_mu;                // guards occ
     std::mutex mu;                    // serialises host-buffer fills on this device
+    std::mutex small_mu;              // serialises users of digest / flag scratch
 };
 
 std::mutex g_ctx_mu;
@@ -128,6 +130,7 @@ int resolve_engine(int engine, int fmt) {
 
 int blocks_per_sm(DevCtx* c, int fmt, int engine, bool interleaved) {
     const int key = (interleaved ? 64 : 0) + fmt * 8 + engine;
+    std::lock_guard<std::mutex> lock(c->occ_mu);
     auto it = c->occ.find(key);
     if (it != c->occ.end()) return it->second;
     const int n = interleaved ? interleaved_blocks_per_sm(fmt, engine, kContigThreads)
@@ -890,6 +893,7 @@ bcn_status bcn_seed_states(const uint64_t* a, const uint64_t* k, uint64_t* out, 
     if (kind != PtrKind::Device) return fail(BCN_ERR_INVALID_ARGUMENT, "seed_states: buffers must be device memory");
     DevCtx* c = nullptr;
     if ((st = get_ctx(dev, &c))) return st;
+    std::lock_guard<std::mutex> scratch_lock(c->small_mu);
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->stream;
     BCN_CUDA(cudaMemsetAsync(c->flag, 0, sizeof(int), s));
     SeedArgs sa{a, k, out, count, steps, c->flag};
@@ -913,6 +917,7 @@ bcn_status bcn_digest(const void* buf, uint64_t n, uint32_t itemsize, uint64_t i
     if (kind != PtrKind::Device) return fail(BCN_ERR_INVALID_ARGUMENT, "digest: buffer must be device memory");
     DevCtx* c = nullptr;
     if ((st = get_ctx(dev, &c))) return st;
+    std::lock_guard<std::mutex> scratch_lock(c->small_mu);
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->stream;
     BCN_CUDA(cudaMemsetAsync(c->digest, 0, 3 * sizeof(unsigned long long), s));
     DigestArgs da{buf, n, itemsize, index_base, c->digest};
@@ -984,6 +989,7 @@ bcn_status bcn_chi_square_uniformity(const double* samples, uint64_t n, int bins
     int dev = device;
     bcn_status st = stage_input(samples, n * sizeof(double), &dev, &in, &c, &s, stream);
     if (st) return st;
+    std::lock_guard<std::mutex> scratch_lock(c->small_mu);
     unsigned long long* counts = nullptr;
     BCN_CUDA(cudaMalloc(&counts, static_cast<size_t>(bins) * 8));
     BCN_CUDA(cudaMemsetAsync(counts, 0, static_cast<size_t>(bins) * 8, s));
@@ -1024,6 +1030,7 @@ bcn_status bcn_monobit_mantissa(const uint64_t* residues, uint64_t n, double* st
     int dev = device;
     bcn_status st = stage_input(residues, n * 8, &dev, &in, &c, &s, stream);
     if (st) return st;
+    std::lock_guard<std::mutex> scratch_lock(c->small_mu);
     unsigned long long* ones = nullptr;
     BCN_CUDA(cudaMalloc(&ones, 53 * 8));
     BCN_CUDA(cudaMemsetAsync(ones, 0, 53 * 8, s));
