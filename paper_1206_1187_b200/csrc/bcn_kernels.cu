@@ -266,21 +266,28 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
         a.rows > first ? static_cast<uint32_t>((a.rows - first + per_round - 1) / per_round) : 0;
     if (rounds == 0) return;  // uniform across the CTA
     if (warp == kWorkers) {
-        // Pacer: release round k no earlier than t0 + k * gap.
+        // Pacer: worker i's store of round k is released no earlier than
+        // t0 + (k + i/8) * gap, through named barrier 1+i shared by the pacer
+        // and worker i only — the CTA's stores are spread over the round
+        // instead of leaving as one burst.
         uint64_t t0 = 0;
         if (lane == 0) t0 = global_ns();
+        const uint64_t sub_q8 = a.gap_q8 / kWorkers;
         for (uint32_t k = 0; k < rounds; ++k) {
-            if (lane == 0 && a.gap_q8) {
-                const uint64_t target = t0 + ((k * a.gap_q8) >> 8);
-                uint64_t now = global_ns();
-                while (now < target) {
-                    const uint64_t d = target - now;
-                    __nanosleep(d > 2048 ? 1024u : static_cast<unsigned>(d >> 1));
-                    now = global_ns();
+#pragma unroll
+            for (int i = 0; i < kWorkers; ++i) {
+                if (lane == 0 && sub_q8) {
+                    const uint64_t target = t0 + (((static_cast<uint64_t>(k) * kWorkers + i) * sub_q8) >> 8);
+                    uint64_t now = global_ns();
+                    while (now < target) {
+                        const uint64_t d = target - now;
+                        __nanosleep(d > 2048 ? 1024u : static_cast<unsigned>(d >> 1));
+                        now = global_ns();
+                    }
                 }
+                __syncwarp();
+                asm volatile("bar.sync %0, 64;" ::"r"(1 + i) : "memory");
             }
-            __syncwarp();
-            asm volatile("bar.sync 1, %0;" ::"n"(kPacedThreads) : "memory");
         }
         return;
     }
@@ -327,7 +334,7 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
                 else
                     bits[h][v] = emit_bits<FMT, E>(st[h][v]);
             }
-        asm volatile("bar.sync 1, %0;" ::"n"(kPacedThreads) : "memory");
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + warp) : "memory");
         if (r + H <= count) {
 #pragma unroll
             for (int h = 0; h < H; ++h) pack_store<FMT>(p + h * hstep, bits[h]);
