@@ -160,6 +160,16 @@ uint64_t paced_grid(const DevCtx* c) {
     return static_cast<uint64_t>(c->sms) * g_pace_cps.load();
 }
 
+// Per-CTA phase offset of the pacing schedule (BCN_PACE_STAGGER=0|1,
+// exploration knob; default 0).
+int pace_stagger() {
+    static const int env = [] {
+        const char* v = std::getenv("BCN_PACE_STAGGER");
+        return v ? static_cast<int>(std::strtol(v, nullptr, 10)) : 0;
+    }();
+    return env;
+}
+
 uint64_t pace_gap_q8(int grid, double gbs, int fmt, bool constant = false) {
     // One round of the grid writes grid * 8 workers * H rows * 1 KiB;
     // 1 GB/s == 1 byte/ns.
@@ -270,6 +280,7 @@ cudaError_t enqueue_affine(const FillJob& j, char* dptr, uint64_t slot0, uint64_
             pa.e0 = c.e0;
             pa.jump = mult_for_steps(static_cast<__int128>(row) * grid * kWorkers * paced_rows_per_round(j.fmt));
             pa.gap_q8 = pace_gap_q8(grid, g_pace_gbs.load(), j.fmt);
+            pa.stagger = pace_stagger();
             pa.mode = kPacedContiguous;
             e = launch_paced(j.fmt, j.engine, pa, grid, j.stream);
         } else {
@@ -335,6 +346,7 @@ cudaError_t enqueue_region(const FillJob& j, char* dptr, uint64_t slot0, uint64_
             pa.rows = rows;
             pa.e0 = r.e0;
             pa.gap_q8 = pace_gap_q8(grid, g_pace_gbs.load(), j.fmt);
+            pa.stagger = pace_stagger();
             pa.mode = kPacedInterleaved;
             pa.q0 = r.q0;
             pa.width = width;
@@ -957,6 +969,7 @@ bcn_status bcn_fill_constant(void* out, uint64_t nbytes, uint64_t pattern, int d
         pa.rows = rows;
         pa.e0 = pattern;
         pa.gap_q8 = pace_gap_q8(grid, g_pace_gbs.load(), kFmtU64, true);
+        pa.stagger = pace_stagger();
         pa.mode = kPacedConstant;
         e = launch_paced(kFmtU64, -1, pa, grid, s);
     } else {

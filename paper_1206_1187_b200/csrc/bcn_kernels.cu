@@ -266,28 +266,28 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
         a.rows > first ? static_cast<uint32_t>((a.rows - first + per_round - 1) / per_round) : 0;
     if (rounds == 0) return;  // uniform across the CTA
     if (warp == kWorkers) {
-        // Pacer: worker i's store of round k is released no earlier than
-        // t0 + (k + i/8) * gap, through named barrier 1+i shared by the pacer
-        // and worker i only — the CTA's stores are spread over the round
-        // instead of leaving as one burst.
+        // Pacer: release round k no earlier than t0 + k * gap (one timer read
+        // and one CTA barrier per round). With `stagger`, each CTA's t0 is
+        // shifted by a golden-ratio fraction of a round so the grid's bursts
+        // are spread over the round instead of leaving together.
         uint64_t t0 = 0;
-        if (lane == 0) t0 = global_ns();
-        const uint64_t sub_q8 = a.gap_q8 / kWorkers;
+        if (lane == 0) {
+            t0 = global_ns();
+            if (a.stagger)
+                t0 += (a.gap_q8 * ((blockIdx.x * 2654435761u) >> 24)) >> 16;
+        }
         for (uint32_t k = 0; k < rounds; ++k) {
-#pragma unroll
-            for (int i = 0; i < kWorkers; ++i) {
-                if (lane == 0 && sub_q8) {
-                    const uint64_t target = t0 + (((static_cast<uint64_t>(k) * kWorkers + i) * sub_q8) >> 8);
-                    uint64_t now = global_ns();
-                    while (now < target) {
-                        const uint64_t d = target - now;
-                        __nanosleep(d > 2048 ? 1024u : static_cast<unsigned>(d >> 1));
-                        now = global_ns();
-                    }
+            if (lane == 0 && a.gap_q8) {
+                const uint64_t target = t0 + ((static_cast<uint64_t>(k) * a.gap_q8) >> 8);
+                uint64_t now = global_ns();
+                while (now < target) {
+                    const uint64_t d = target - now;
+                    __nanosleep(d > 2048 ? 1024u : static_cast<unsigned>(d >> 1));
+                    now = global_ns();
                 }
-                __syncwarp();
-                asm volatile("bar.sync %0, 64;" ::"r"(1 + i) : "memory");
             }
+            __syncwarp();
+            asm volatile("bar.sync 1, %0;" ::"n"(kPacedThreads) : "memory");
         }
         return;
     }
@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
                 else
                     bits[h][v] = emit_bits<FMT, E>(st[h][v]);
             }
-        asm volatile("bar.sync %0, 64;" ::"r"(1 + warp) : "memory");
+        asm volatile("bar.sync 1, %0;" ::"n"(kPacedThreads) : "memory");
         if (r + H <= count) {
 #pragma unroll
             for (int h = 0; h < H; ++h) pack_store<FMT>(p + h * hstep, bits[h]);
