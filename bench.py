@@ -311,11 +311,16 @@ def main() -> None:
     const_per, _, _ = timed(lambda: B.device.fill_constant(raw, stream=stream),
                             max(20, args.steps // 4), 5)
     const_gbs = buf_items * isz / (statistics.mean(const_per) * 1e-3) / 1e9
-    pace_now = lib.bcn_write_pacing()
-    lib.bcn_set_write_pacing(0.0, 2, 3)
+    pace_now = B.device.write_pacing_config()
+    lib.bcn_set_write_pacing(0.0, pace_now[1], pace_now[2])
     const_per_u, _, _ = timed(lambda: B.device.fill_constant(raw, stream=stream),
                               max(20, args.steps // 4), 5)
-    lib.bcn_set_write_pacing(pace_now, 2, 3)
+    lib.bcn_set_write_pacing(*pace_now)
+    # The same paced writer with random words: toggles the HBM interface like
+    # real output (a constant pattern draws ~230 W less at 7 TB/s), so under
+    # the board power cap this is the realistic write ceiling.
+    noise_per, _, _ = timed(lambda: B.device.fill_noise(raw, stream=stream), args.steps, 5)
+    noise_gbs = buf_items * isz / (statistics.mean(noise_per) * 1e-3) / 1e9
     const_unpaced_gbs = buf_items * isz / (statistics.mean(const_per_u) * 1e-3) / 1e9
 
 
@@ -392,6 +397,7 @@ def main() -> None:
                 "workload": workload, "items_per_step": total_items, "format": args.fmt,
                 "engine": B.par.Engine(resolved).name, "layout": "contiguous",
                 "write_pacing_gbs": pace if (pace > 0 and isz == 8) else None,
+                "write_pacing_ctas_per_sm": B.device.write_pacing_config()[1],
                 "parallelism": f"index-sharded x{world}, no data-path collective",
                 "l2": f"output {buf_items * isz / 2**30:.0f} GiB per launch >> 126 MB L2 "
                       "(inputs larger than L2, no flush needed)",
@@ -407,6 +413,8 @@ def main() -> None:
                          "constant_writer_gbs": const_gbs,
                          "constant_writer_unpaced_gbs": const_unpaced_gbs,
                          "frac_of_constant_writer": achieved_gbs / const_gbs,
+                         "noise_writer_gbs": noise_gbs,
+                         "frac_of_noise_writer": achieved_gbs / noise_gbs,
                          "note": "peak = measured STREAM copy (read+write); pure HBM writes reach "
                                  "~7.4 TB/s on this part (CE memset 7.39, paced Constant writer "
                                  "7.3-7.47: profiles/r01), so frac can exceed 1"},

@@ -143,6 +143,13 @@ bcn_status bcn_digest(const void* buf, uint64_t n, uint32_t itemsize, uint64_t i
 bcn_status bcn_fill_constant(void* out, uint64_t nbytes, uint64_t pattern, int device,
                              void* stream);
 
+/* Write-ceiling probe: the Constant writer's geometry and write pacing, but
+ * each thread writes fixed pseudo-random words derived from `seed` (non-zero)
+ * — data that toggles the HBM interface like generator output, which costs
+ * measurably more power than a constant pattern. Same pointer rules and
+ * stream semantics as bcn_fill_constant. Not part of the reference API. */
+bcn_status bcn_fill_noise(void* out, uint64_t nbytes, uint64_t seed, int device, void* stream);
+
 /* Engine AUTO resolves to this engine for (format); exposed for benches. */
 int bcn_auto_engine(bcn_format format);
 
@@ -159,12 +166,15 @@ bcn_status bcn_set_launch_config(int ctas_per_sm, int row_order);
 /* Process-wide HBM write pacing of the contiguous fill and Constant kernels.
  * B200 write efficiency drops when SM stores oversubscribe HBM; the paced
  * kernels meter their stores to `target_gbs` (GB/s, per device) with one pacer
- * warp per CTA reading %globaltimer. 0 disables pacing. ctas_per_sm in [1,7];
+ * warp per CTA reading %globaltimer. 0 disables pacing. ctas_per_sm in [1,7]
+ * (default 1: 8 worker warps per SM — measured ~1.3% faster sustained than 2);
  * format_mask: bit f enables pacing for bcn_format f (default U64|F64 = 3).
  * Output bits never depend on it. */
 bcn_status bcn_set_write_pacing(double target_gbs, int ctas_per_sm, int format_mask);
 /* Current pacing target in GB/s (0 = unpaced). */
 double bcn_write_pacing(void);
+/* Current pacing configuration (any pointer may be NULL). */
+void bcn_get_write_pacing(double* target_gbs, int* ctas_per_sm, int* format_mask);
 
 /* ---- quality.hpp: statistical smoke suite on the GPU ---
  * Host or device input pointers. Preconditions and formulas follow

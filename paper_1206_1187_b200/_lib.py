@@ -32,6 +32,8 @@ SIGNATURES = [
     ("bcn_launch_count", _u64, []),
     ("bcn_set_launch_config", _int, [_int, _int]),
     ("bcn_set_write_pacing", _int, [ctypes.c_double, _int, _int]),
+    ("bcn_get_write_pacing", None, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_int),
+                                    ctypes.POINTER(_int)]),
     ("bcn_write_pacing", ctypes.c_double, []),
     ("bcn_modpow2", _int, [_u64, _u64, _pu64]),
     ("bcn_seed_from_index", _int, [_u64, _pu64]),
@@ -47,6 +49,7 @@ SIGNATURES = [
     ("bcn_seed_states", _int, [_vp, _vp, _vp, _u64, _u32, _int, _vp]),
     ("bcn_digest", _int, [_vp, _u64, _u32, _u64, _pu64, _int, _vp]),
     ("bcn_fill_constant", _int, [_vp, _u64, _u64, _int, _vp]),
+    ("bcn_fill_noise", _int, [_vp, _u64, _u64, _int, _vp]),
     ("bcn_format_text", _int, [_vp, _u64, _vp, _u64, _pu64]),
     ("bcn_chi_square_uniformity", _int, [_vp, _u64, _int, ctypes.POINTER(ctypes.c_double),
                                          ctypes.POINTER(_int), ctypes.POINTER(_int), _int, _vp]),

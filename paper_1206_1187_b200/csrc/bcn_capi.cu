@@ -146,7 +146,7 @@ std::atomic<int> g_row_order{1};
 // Write pacing (bcn_set_write_pacing): target HBM write rate of the paced
 // contiguous kernels in GB/s (0 = unpaced) and their CTAs per SM.
 std::atomic<double> g_pace_gbs{kDefaultPaceGBs};
-std::atomic<int> g_pace_cps{2};
+std::atomic<int> g_pace_cps{kDefaultPaceCps};
 std::atomic<int> g_pace_formats{(1 << kFmtU64) | (1 << kFmtF64)};
 
 // CTAs of the paced grid: ctas_per_sm x SMs, or BCN_PACE_GRID (an
@@ -695,6 +695,12 @@ bcn_status bcn_set_write_pacing(double target_gbs, int ctas_per_sm, int format_m
 
 double bcn_write_pacing(void) { return g_pace_gbs.load(); }
 
+void bcn_get_write_pacing(double* target_gbs, int* ctas_per_sm, int* format_mask) {
+    if (target_gbs) *target_gbs = g_pace_gbs.load();
+    if (ctas_per_sm) *ctas_per_sm = g_pace_cps.load();
+    if (format_mask) *format_mask = g_pace_formats.load();
+}
+
 bcn_status bcn_set_launch_config(int ctas_per_sm, int row_order) {
     if (ctas_per_sm < 0 || ctas_per_sm > 32 || row_order < 0 || row_order > 1)
         return fail(BCN_ERR_INVALID_ARGUMENT, "set_launch_config: ctas_per_sm in [0,32], row_order 0|1");
@@ -945,20 +951,23 @@ bcn_status bcn_digest(const void* buf, uint64_t n, uint32_t itemsize, uint64_t i
     return BCN_OK;
 }
 
-bcn_status bcn_fill_constant(void* out, uint64_t nbytes, uint64_t pattern, int device, void* stream) {
-    if (!out) return fail(BCN_ERR_INVALID_ARGUMENT, "fill_constant: null buffer");
+namespace {
+// The Constant writer and its noise variant (bcn_fill_constant / bcn_fill_noise).
+bcn_status constant_writer(const char* what, void* out, uint64_t nbytes, uint64_t pattern,
+                           uint64_t noise_seed, int device, void* stream) {
+    if (!out) return fail(BCN_ERR_INVALID_ARGUMENT, std::string(what) + ": null buffer");
     if (reinterpret_cast<uintptr_t>(out) % 32 || nbytes % 1024)
-        return fail(BCN_ERR_INVALID_ARGUMENT, "fill_constant: needs 32-byte alignment and whole 1 KiB rows");
+        return fail(BCN_ERR_INVALID_ARGUMENT, std::string(what) + ": needs 32-byte alignment and whole 1 KiB rows");
     int dev = device;
     PtrKind kind;
     bcn_status st = classify(out, &dev, &kind);
     if (st) return st;
-    if (kind != PtrKind::Device) return fail(BCN_ERR_INVALID_ARGUMENT, "fill_constant: buffer must be device memory");
+    if (kind != PtrKind::Device) return fail(BCN_ERR_INVALID_ARGUMENT, std::string(what) + ": buffer must be device memory");
     DevCtx* c = nullptr;
     if ((st = get_ctx(dev, &c))) return st;
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->stream;
     cudaError_t e;
-    if (g_pace_gbs.load() > 0.0) {
+    if (g_pace_gbs.load() > 0.0 || noise_seed) {
         // The Constant writer under the same metering as the paced fill.
         constexpr uint64_t kWorkers = kPacedThreads / 32 - 1;
         const uint64_t rows = nbytes / 1024;
@@ -968,18 +977,29 @@ bcn_status bcn_fill_constant(void* out, uint64_t nbytes, uint64_t pattern, int d
         pa.out = out;
         pa.rows = rows;
         pa.e0 = pattern;
-        pa.gap_q8 = pace_gap_q8(grid, g_pace_gbs.load(), kFmtU64, true);
+        pa.gap_q8 = g_pace_gbs.load() > 0.0 ? pace_gap_q8(grid, g_pace_gbs.load(), kFmtU64, true) : 0;
         pa.stagger = pace_stagger();
         pa.mode = kPacedConstant;
+        pa.q0 = noise_seed;  // != 0: per-thread pseudo-random words instead of `pattern`
         e = launch_paced(kFmtU64, -1, pa, grid, s);
     } else {
         ConstArgs ca{out, nbytes / 1024, pattern, static_cast<uint32_t>(g_row_order.load())};
         const int grid = grid_for_rows(c, kFmtF64, kEngBarrett, false, ca.rows);
         e = launch_constant(ca, grid, kContigThreads, s);
     }
-    if (e != cudaSuccess) return cuda_fail(e, "fill_constant launch");
+    if (e != cudaSuccess) return cuda_fail(e, what);
     if (!stream) BCN_CUDA(cudaStreamSynchronize(s));
     return BCN_OK;
+}
+}  // namespace
+
+bcn_status bcn_fill_constant(void* out, uint64_t nbytes, uint64_t pattern, int device, void* stream) {
+    return constant_writer("fill_constant", out, nbytes, pattern, 0, device, stream);
+}
+
+bcn_status bcn_fill_noise(void* out, uint64_t nbytes, uint64_t seed, int device, void* stream) {
+    if (seed == 0) return fail(BCN_ERR_INVALID_ARGUMENT, "fill_noise: seed must be non-zero");
+    return constant_writer("fill_noise", out, nbytes, 0, seed, device, stream);
 }
 
 }  // extern "C"

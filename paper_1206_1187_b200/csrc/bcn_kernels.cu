@@ -296,6 +296,22 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
     const uint32_t count = a.rows > w ? static_cast<uint32_t>((a.rows - w + nwk - 1) / nwk) : 0;
     typename E::State st[H][V];
     uint64_t col[INTER ? H : 1][INTER ? V : 1];  // interleaved: worker index of each stream's slot
+    // Constant writer pattern: a.e0 everywhere, or (a.q0 != 0, exploration)
+    // fixed per-thread random words, to separate data-toggling power from
+    // generator power.
+    uint64_t pat[CONST ? H : 1][CONST ? V : 1];
+    if constexpr (CONST) {
+#pragma unroll
+        for (int h = 0; h < H; ++h)
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                uint64_t x = a.q0 + 0x9e3779b97f4a7c15ull *
+                                        ((static_cast<uint64_t>(blockIdx.x) * kPacedThreads + threadIdx.x) * (H * V) + h * V + v + 1);
+                x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+                x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+                pat[h][v] = a.q0 ? (x ^ (x >> 31)) : a.e0;
+            }
+    }
     if (!CONST) {
 #pragma unroll
         for (int h = 0; h < H; ++h) {
@@ -330,7 +346,7 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
 #pragma unroll
             for (int v = 0; v < V; ++v) {
                 if constexpr (CONST)
-                    bits[h][v] = a.e0;
+                    bits[h][v] = pat[h][v];
                 else
                     bits[h][v] = emit_bits<FMT, E>(st[h][v]);
             }

@@ -174,6 +174,10 @@ __host__ __device__ constexpr int paced_rows_per_round(int fmt, bool constant = 
 // profiles/r01/tune_pace.jsonl): FP64 engine f64/u64 reach ~7.08 TB/s at
 // 7200 vs ~6.25 unpaced; above ~7.3 the write path starts to oversubscribe.
 constexpr double kDefaultPaceGBs = 7200.0;
+// CTAs per SM of the paced grid: 1 and 2 reach the same single-launch rate;
+// under the board power cap 1 is ~1.3% faster sustained (profiles/r01/
+// timeline_cps_pace.jsonl).
+constexpr int kDefaultPaceCps = 1;
 constexpr int kBulkTileRows = 16;  // 16 KiB per TMA bulk store
 constexpr int kBulkStages = 3;     // tiles in flight per CTA
 

@@ -3,6 +3,7 @@
 * :func:`seed_states` — batched skip-ahead seeding kernel.
 * :func:`digest` — order-sensitive checksums of a device buffer.
 * :func:`fill_constant` — the Constant writer, the write-roofline denominator.
+* :func:`fill_noise` — the Constant writer with random data (power-realistic ceiling).
 * :func:`fill_multi` — one-process multi-GPU fill over contiguous shards.
 """
 from __future__ import annotations
@@ -62,6 +63,14 @@ def fill_constant(buf: torch.Tensor, pattern: int = 0x3FE0000000000000, stream=N
               pattern, buf.device.index, _stream(buf, stream))
 
 
+def fill_noise(buf: torch.Tensor, seed: int = 0x1206_1187, stream=None) -> None:
+    """The Constant writer writing fixed per-thread pseudo-random words (the
+    power-realistic write ceiling). Asynchronous on the current torch stream."""
+    _cuda(buf, "fill_noise")
+    _lib.call("bcn_fill_noise", ctypes.c_void_p(buf.data_ptr()), buf.numel() * buf.element_size(),
+              seed, buf.device.index, _stream(buf, stream))
+
+
 def fill_multi(outs: list[torch.Tensor], n: int, seed_index: int = kMinSeedIndex,
                base_offset: int = 0, fmt: Format = Format.F64,
                engine: Engine = Engine.Auto) -> None:
@@ -80,7 +89,7 @@ def set_launch_config(ctas_per_sm: int = 0, row_order: int = 1) -> None:
     _lib.call("bcn_set_launch_config", ctas_per_sm, row_order)
 
 
-def set_write_pacing(target_gbs: float, ctas_per_sm: int = 2, format_mask: int = 3) -> None:
+def set_write_pacing(target_gbs: float, ctas_per_sm: int = 1, format_mask: int = 3) -> None:
     """Meter the contiguous fill / Constant stores to `target_gbs` per device
     (0 = unpaced) for the formats in `format_mask` (bit = Format value);
     see bcn_set_write_pacing."""
@@ -89,6 +98,13 @@ def set_write_pacing(target_gbs: float, ctas_per_sm: int = 2, format_mask: int =
 
 def write_pacing() -> float:
     return float(_lib.lib().bcn_write_pacing())
+
+
+def write_pacing_config() -> tuple[float, int, int]:
+    """(target GB/s, CTAs per SM, format mask) of the current write pacing."""
+    g, c, m = ctypes.c_double(), ctypes.c_int(), ctypes.c_int()
+    _lib.lib().bcn_get_write_pacing(ctypes.byref(g), ctypes.byref(c), ctypes.byref(m))
+    return g.value, c.value, m.value
 
 
 def auto_engine(fmt: Format = Format.F64) -> Engine:

@@ -169,7 +169,7 @@ def test_seed_extremes(bcn, cuda, oracle):
 def test_paced_kernels_bit_exact(bcn, cuda, oracle, pace):
     """The write-paced contiguous kernels (pacer warp + named barrier) produce
     the same bits as every other path, for all engines and formats."""
-    old = bcn.device.write_pacing()
+    old = bcn.device.write_pacing_config()
     try:
         bcn.device.set_write_pacing(pace, 2, 7)
         for engine in ("Barrett", "Montgomery", "FP64", "Mixed"):
@@ -182,7 +182,7 @@ def test_paced_kernels_bit_exact(bcn, cuda, oracle, pace):
         torch.cuda.synchronize()
         assert bool((c == 0.5).all())
     finally:
-        bcn.device.set_write_pacing(old, 2, 3)
+        bcn.device.set_write_pacing(*old)
 
 
 # ------------------------------------------------------------- host buffers
@@ -255,6 +255,29 @@ def test_digest_and_constant(bcn, cuda, oracle):
     bcn.device.fill_constant(c)
     torch.cuda.synchronize()
     assert bool((c == 0.5).all())
+
+
+def test_fill_noise_writer(bcn, cuda):
+    """The noise writer covers the whole buffer with seed-determined, non-constant
+    words, paced or not; a zero seed is rejected."""
+    c = torch.zeros(1 << 21, dtype=torch.int64, device=cuda)
+    d = torch.zeros_like(c)
+    old = bcn.device.write_pacing_config()
+    try:
+        for pace in (0.0, 7000.0):
+            bcn.device.set_write_pacing(pace, 2, 3)
+            c.zero_()
+            d.zero_()
+            bcn.device.fill_noise(c, seed=7)
+            bcn.device.fill_noise(d, seed=7)
+            torch.cuda.synchronize()
+            assert int((c == 0).sum()) == 0
+            assert torch.equal(c, d)
+            assert c.unique().numel() > 10000
+    finally:
+        bcn.device.set_write_pacing(*old)
+    with pytest.raises(bcn.InvalidArgument):
+        bcn.device.fill_noise(c, seed=0)
 
 
 def test_fill_multi_concatenation(bcn, cuda, oracle):

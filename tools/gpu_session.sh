@@ -1,7 +1,14 @@
+# Scratch driver for one gpurun call (edited per experiment).
 set -x
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw,temperature.gpu --format=csv
-timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -15 > gpurun_out/pytest_gpu.log
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -5 > gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
-for s in 1 0 1 0; do BCN_PACE_STAGGER=$s timeout 300 python bench.py --no-cpu > gpurun_out/bench_stagger$s.$RANDOM.json 2>gpurun_out/bench_err.log; done
-for s in 1 0; do BCN_PACE_STAGGER=$s timeout 600 python tools/tune.py --fmts f64 --engines FP64 --pace 6800,7000,7200,7400,7600 --cps 2 --rounds 4 > gpurun_out/tune_stagger$s.jsonl 2>&1; done
-timeout 300 python bench.py > gpurun_out/bench_default.json 2>>gpurun_out/bench_err.log
+timeout 300 python bench.py > gpurun_out/bench1.json 2>>gpurun_out/err.log
+timeout 300 python bench.py --impl reference > gpurun_out/bench_ref.json 2>>gpurun_out/err.log
+timeout 300 python bench.py > gpurun_out/bench2.json 2>>gpurun_out/err.log
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_bench.csv python bench.py --steps 20 --warmup 3 --no-cpu > gpurun_out/bench_under_ncu.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -o /tmp/prof_all python tools/profile_all.py > gpurun_out/prof_all.log 2>&1
+python tools/ncu_summary.py /tmp/prof_all.ncu-rep -o gpurun_out/ncu_full_all_kernels.json >> gpurun_out/prof_all.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_fill_paced -c 1 -o gpurun_out/prof_paced python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e > gpurun_out/prof_paced.log 2>&1
+ncu -i gpurun_out/prof_paced.ncu-rep --page source --csv > gpurun_out/prof_paced_source.csv 2>&1
+nproc > gpurun_out/nproc.txt
+du -sh gpurun_out

@@ -43,6 +43,7 @@ def main() -> None:
         ("paced interleaved W=7", lambda: fill(f64, B.Format.F64,
                                                p=B.par.make_plan(n, 7, B.Layout.Interleaved))),
         ("paced constant", lambda: B.device.fill_constant(u64)),
+        ("paced noise writer", lambda: B.device.fill_noise(u64)),
     ]
     unpaced = [
         ("contig f64 FP64 unpaced", lambda: fill(f64, B.Format.F64, B.Engine.FP64)),
@@ -58,13 +59,13 @@ def main() -> None:
         sync()
         fn()
         sync()
-    B.device.set_write_pacing(0, 2, 3)
+    B.device.set_write_pacing(0, 1, 3)
     for name, fn in unpaced:
         fn()
         sync()
         fn()
         sync()
-    B.device.set_write_pacing(7200, 2, 3)
+    B.device.set_write_pacing(7200, 1, 3)
     # small / auxiliary kernels
     small = torch.empty(100003 + 1, dtype=torch.float64, device=dev)[1:]
     B.par.fill(small, B.par.make_plan(100003, 3), A0, base_offset=(1 << 64) - 50000)  # slots (wrap)
