@@ -870,25 +870,18 @@ bcn_status bcn_deinterleave(const void* in, void* out, uint64_t n, uint32_t work
     t.wpw = p.wpw;
     t.itemsize = itemsize;
     // Region 1: rows [0, sc) of all workers; region 2: the remaining
-    // wpw - sc elements of workers 0..W-2 (parallel.cpp:24-33). Rows are
-    // processed in launches of at most 65535*32.
+    // wpw - sc elements of workers 0..W-2 (parallel.cpp:24-33). One
+    // persistent-grid launch per region.
     for (int region = 0; region < 2; ++region) {
         const uint64_t rows = region == 0 ? sc : p.wpw - sc;
         const uint64_t width = region == 0 ? p.workers : p.workers - 1;
-        const uint64_t p0 = region == 0 ? 0 : sc * p.workers;
-        const uint64_t ib = region == 0 ? 0 : sc;
         if (rows == 0 || width == 0) continue;
-        // The wide kernel's 2D grid caps a launch at 65535*32 rows; the narrow
-        // kernel (width <= 32) is grid-strided and takes the region whole.
-        const uint64_t max_rows = width <= 32 ? rows : 65535ull * 32;
-        for (uint64_t r0 = 0; r0 < rows; r0 += max_rows) {
-            t.p0 = p0 + r0 * width;
-            t.rows = std::min(max_rows, rows - r0);
-            t.width = width;
-            t.i_base = ib + r0;
-            cudaError_t e = launch_transpose(t, s);
-            if (e != cudaSuccess) return cuda_fail(e, "deinterleave launch");
-        }
+        t.p0 = region == 0 ? 0 : sc * p.workers;
+        t.rows = rows;
+        t.width = width;
+        t.i_base = region == 0 ? 0 : sc;
+        cudaError_t e = launch_transpose(t, s);
+        if (e != cudaSuccess) return cuda_fail(e, "deinterleave launch");
     }
     if (tmp) {
         BCN_CUDA(cudaMemcpyAsync(out, dout, bytes, cudaMemcpyDeviceToHost, s));

@@ -705,52 +705,156 @@ __global__ void __launch_bounds__(kContigThreads) k_constant(const ConstArgs a) 
 // Device deinterleave of one Interleaved region: the region is a row-major
 // [rows x width] matrix M[i][w] at physical slot p0; logical position of
 // M[i][w] is w*wpw + i_base + i. 32x32 smem tiles keep both sides coalesced.
-template <typename T>
-__global__ void __launch_bounds__(256) k_transpose(const TransposeArgs a) {
-    __shared__ T tile[32][33];
+// Both kernels are persistent and software-pipelined: the next tile's loads
+// are issued into registers before the current tile is written out of shared
+// memory, so every SM keeps reads and writes in flight at once.
+//
+// Wide regions (width > kNarrowMaxWidth workers): 64-row x 512-byte tiles of
+// the [rows x width] region (64 workers of u64, 128 of u32). Loads run along
+// tile rows (512-byte runs of the input, 16 or 32 per thread), the tile sits in
+// shared memory with an odd pitch (conflict-free column reads for 4- and
+// 8-byte items), and stores run along tile columns: each worker's 64
+// consecutive logical items leave as one run.
+constexpr unsigned kNarrowMaxWidth = 128;
+
+template <typename T, int ROWS = 64, int BYTES = 512>
+struct WideTile {
+    static constexpr int kRows = ROWS;
+    static constexpr int kCols = BYTES / static_cast<int>(sizeof(T));  // workers
+    static constexpr int kPitch = kCols + 1;
+    static constexpr int kLoads = kRows * kCols / 256;                // per thread
+    static_assert(kCols <= 256 && 256 % kCols == 0 && kRows % (256 / kCols) == 0, "tile shape");
+};
+
+template <typename T, class G>
+__device__ __forceinline__ void wide_load(const TransposeArgs& a, uint64_t t, uint64_t ntw,
+                                          T (&v)[G::kLoads]) {
     const T* in = static_cast<const T*>(a.in);
-    T* out = static_cast<T*>(a.out);
-    const uint64_t i0 = static_cast<uint64_t>(blockIdx.y) * 32;  // region row (element)
-    const uint64_t w0 = static_cast<uint64_t>(blockIdx.x) * 32;  // worker
-    for (int dy = threadIdx.y; dy < 32; dy += 8) {
-        const uint64_t i = i0 + dy, w = w0 + threadIdx.x;
-        if (i < a.rows && w < a.width) tile[dy][threadIdx.x] = in[a.p0 + i * a.width + w];
-    }
-    __syncthreads();
-    for (int dy = threadIdx.y; dy < 32; dy += 8) {
-        const uint64_t w = w0 + dy, i = i0 + threadIdx.x;
-        if (i < a.rows && w < a.width) out[w * a.wpw + a.i_base + i] = tile[threadIdx.x][dy];
+    const uint64_t w0 = (t % ntw) * G::kCols, i0 = (t / ntw) * G::kRows;
+    const T* src = in + a.p0 + i0 * a.width + w0;
+    constexpr int kRowStep = 256 / G::kCols;  // rows a thread advances per load
+    const int r = threadIdx.x / G::kCols, c = threadIdx.x % G::kCols;
+    if (w0 + G::kCols <= a.width && i0 + G::kRows <= a.rows) {
+        const T* p = src + static_cast<uint64_t>(r) * a.width + c;
+        const uint64_t step = kRowStep * a.width;
+#pragma unroll
+        for (int j = 0; j < G::kLoads; ++j) v[j] = p[j * step];
+    } else {
+#pragma unroll
+        for (int j = 0; j < G::kLoads; ++j) {
+            const int rr = r + kRowStep * j;
+            v[j] = (i0 + rr < a.rows && w0 + c < a.width) ? src[static_cast<uint64_t>(rr) * a.width + c] : T(0);
+        }
     }
 }
 
-// Narrow regions (width <= 32 workers): a CTA takes R consecutive rows of the
-// [rows x width] region (R*width <= kNarrowTile slots, read as one contiguous
-// span: thread t reads row t's `width` items, so a warp covers 32*width
-// consecutive items and every sector it touches is fully used), transposes them
-// into shared memory as [width][R] with an odd pitch (conflict-free), and
-// writes each worker's R consecutive logical items with coalesced stores.
-constexpr int kNarrowTile = 4096;
+template <typename T, int ROWS, int BYTES>
+__global__ void __launch_bounds__(256) k_transpose(const TransposeArgs a) {
+    using G = WideTile<T, ROWS, BYTES>;
+    extern __shared__ __align__(16) unsigned char wide_smem[];
+    T* tile = reinterpret_cast<T*>(wide_smem);
+    T* out = static_cast<T*>(a.out);
+    const uint64_t ntw = (a.width + G::kCols - 1) / G::kCols;
+    const uint64_t ntiles = ntw * ((a.rows + G::kRows - 1) / G::kRows);
+    constexpr int kRowStep = 256 / G::kCols;
+    const int r = threadIdx.x / G::kCols, c = threadIdx.x % G::kCols;
+    T v[G::kLoads];
+    uint64_t t = blockIdx.x;
+    if (t < ntiles) wide_load<T, G>(a, t, ntw, v);
+    for (; t < ntiles; t += gridDim.x) {
+#pragma unroll
+        for (int j = 0; j < G::kLoads; ++j) tile[(r + kRowStep * j) * G::kPitch + c] = v[j];
+        __syncthreads();
+        if (t + gridDim.x < ntiles) wide_load<T, G>(a, t + gridDim.x, ntw, v);  // prefetch
+        const uint64_t w0 = (t % ntw) * G::kCols, i0 = (t / ntw) * G::kRows;
+        T* dst = out + w0 * a.wpw + a.i_base + i0;
+        const int i = threadIdx.x % G::kRows;  // item within the worker's run
+        const int wq = threadIdx.x / G::kRows;  // first worker of this thread
+        if (w0 + G::kCols <= a.width && i0 + G::kRows <= a.rows) {
+#pragma unroll 8
+            for (int wl = wq; wl < G::kCols; wl += 256 / G::kRows)
+                dst[wl * a.wpw + i] = tile[i * G::kPitch + wl];
+        } else {
+            for (int wl = wq; wl < G::kCols; wl += 256 / G::kRows)
+                if (w0 + wl < a.width && i0 + i < a.rows) dst[wl * a.wpw + i] = tile[i * G::kPitch + wl];
+        }
+        __syncthreads();
+    }
+}
+
+// Narrow regions (width <= kNarrowMaxWidth workers): tiles of R whole rows
+// (R*width <= kNarrowItems slots, R a multiple of 64) are one contiguous span
+// of the input, read fully coalesced (kNarrowItems/256 loads per thread),
+// scattered into shared memory as [width][R] with an odd pitch (row = slot /
+// width by a multiply-high), and each worker's R consecutive logical items
+// leave as one run (all warps on one worker for width < 8, one worker per
+// warp otherwise).
+template <typename T>
+struct NarrowTile {
+    static constexpr unsigned kItems = 8192;  // slots per tile (64 / 32 KiB)
+    static constexpr unsigned kLoads = kItems / 256;
+};
+
+template <typename T>
+__device__ __forceinline__ void narrow_load(const TransposeArgs& a, uint64_t r0, unsigned items,
+                                            T (&v)[NarrowTile<T>::kLoads]) {
+    using G = NarrowTile<T>;
+    const T* src = static_cast<const T*>(a.in) + a.p0 + r0 * a.width;
+    if (items == G::kItems) {
+#pragma unroll
+        for (unsigned j = 0; j < G::kLoads; ++j) v[j] = src[threadIdx.x + 256 * j];
+    } else {
+#pragma unroll
+        for (unsigned j = 0; j < G::kLoads; ++j) {
+            const unsigned q = threadIdx.x + 256 * j;
+            v[j] = q < items ? src[q] : T(0);
+        }
+    }
+}
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_transpose_narrow(const TransposeArgs a) {
-    __shared__ T tile[kNarrowTile + 32];
-    const T* in = static_cast<const T*>(a.in);
+    using G = NarrowTile<T>;
+    extern __shared__ __align__(16) unsigned char narrow_smem[];
+    T* tile = reinterpret_cast<T*>(narrow_smem);
     T* out = static_cast<T*>(a.out);
-    const unsigned width = static_cast<unsigned>(a.width);
-    unsigned R = kNarrowTile / width;
-    R = R > 256 ? 256 : R;           // one row per thread
-    const unsigned pitch = R | 1;    // odd pitch: w-major writes hit distinct banks
-    for (uint64_t r0 = static_cast<uint64_t>(blockIdx.x) * R; r0 < a.rows;
-         r0 += static_cast<uint64_t>(gridDim.x) * R) {
-        const unsigned nr = static_cast<unsigned>(a.rows - r0 < R ? a.rows - r0 : R);
-        if (threadIdx.x < nr) {
-            const T* src = in + a.p0 + (r0 + threadIdx.x) * width;
-            for (unsigned w = 0; w < width; ++w) tile[w * pitch + threadIdx.x] = src[w];
+    const unsigned W = static_cast<unsigned>(a.width);
+    const unsigned R = G::kItems / W / 64 * 64;  // rows per tile
+    const unsigned P = R | 1;                      // odd pitch
+    // slot / W == (slot * M) >> 32 exactly for slot < 2^32 / W, M = ceil(2^32 / W)
+    const uint64_t M = ((1ull << 32) + W - 1) / W;
+    const uint64_t ntiles = (a.rows + R - 1) / R;
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    auto rows_of = [&](uint64_t t) {
+        return static_cast<unsigned>(a.rows - t * R < R ? a.rows - t * R : R);
+    };
+    T v[G::kLoads];
+    uint64_t t = blockIdx.x;
+    if (t < ntiles) narrow_load<T>(a, t * R, rows_of(t) * W, v);
+    for (; t < ntiles; t += gridDim.x) {
+        const unsigned nr = rows_of(t), items = nr * W;
+#pragma unroll
+        for (unsigned j = 0; j < G::kLoads; ++j) {
+            const unsigned q = threadIdx.x + 256 * j;
+            if (q < items) {
+                const unsigned row = static_cast<unsigned>((q * M) >> 32);
+                tile[(q - row * W) * P + row] = v[j];
+            }
         }
         __syncthreads();
-        for (unsigned w = 0; w < width; ++w) {
-            T* dst = out + w * a.wpw + a.i_base + r0;
-            for (unsigned i = threadIdx.x; i < nr; i += blockDim.x) dst[i] = tile[w * pitch + i];
+        const uint64_t tn = t + gridDim.x;
+        if (tn < ntiles) narrow_load<T>(a, tn * R, rows_of(tn) * W, v);  // prefetch
+        T* dst = out + a.i_base + t * R;
+        if (W < 8) {
+            for (unsigned col = 0; col < W; ++col)
+                for (unsigned i = threadIdx.x; i < nr; i += 256) dst[col * a.wpw + i] = tile[col * P + i];
+        } else {
+            for (unsigned col = warp; col < W; col += 8) {
+                T* d = dst + col * a.wpw;
+                const T* s = tile + col * P;
+#pragma unroll 4
+                for (unsigned i = lane; i < nr; i += 32) d[i] = s[i];
+            }
         }
         __syncthreads();
     }
@@ -955,31 +1059,49 @@ cudaError_t launch_constant(const ConstArgs& a, int grid, int block, cudaStream_
     return counted(cudaGetLastError());
 }
 
-cudaError_t launch_transpose(const TransposeArgs& a, cudaStream_t s) {
-    if (a.rows == 0 || a.width == 0) return cudaSuccess;
-    if (a.width <= 32) {
-        const uint64_t per = std::min<uint64_t>(256, kNarrowTile / a.width);
-        const uint64_t tiles = (a.rows + per - 1) / per;
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const uint64_t cap = static_cast<uint64_t>(sms) * 8;
-        const unsigned grid = static_cast<unsigned>(tiles < cap ? tiles : cap);
-        if (a.itemsize == 8)
-            k_transpose_narrow<uint64_t><<<grid, 256, 0, s>>>(a);
-        else
-            k_transpose_narrow<uint32_t><<<grid, 256, 0, s>>>(a);
-        return counted(cudaGetLastError());
-    }
-    const dim3 grid(static_cast<unsigned>((a.width + 31) / 32), static_cast<unsigned>((a.rows + 31) / 32));
-    if (grid.y > 65535u) return cudaErrorInvalidValue;
-    const dim3 block(32, 8);
-    if (a.itemsize == 8) {
-        k_transpose<uint64_t><<<grid, block, 0, s>>>(a);
+namespace {
+template <typename T, int ROWS, int BYTES>
+cudaError_t transpose_wide(const TransposeArgs& a, int sms, cudaStream_t s) {
+    using G = WideTile<T, ROWS, BYTES>;
+    const size_t smem = static_cast<size_t>(G::kRows) * G::kPitch * sizeof(T);
+    cudaFuncSetAttribute(k_transpose<T, ROWS, BYTES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    const uint64_t tiles = ((a.width + G::kCols - 1) / G::kCols) * ((a.rows + G::kRows - 1) / G::kRows);
+    const uint64_t cap = static_cast<uint64_t>(sms) * occupancy(k_transpose<T, ROWS, BYTES>, 256, smem);
+    k_transpose<T, ROWS, BYTES><<<static_cast<unsigned>(std::min(tiles, cap)), 256, smem, s>>>(a);
+    return counted(cudaGetLastError());
+}
+
+template <typename T>
+cudaError_t transpose_t(const TransposeArgs& a, cudaStream_t s) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (a.width <= kNarrowMaxWidth) {
+        using G = NarrowTile<T>;
+        const size_t smem = (G::kItems + kNarrowMaxWidth) * sizeof(T);
+        cudaFuncSetAttribute(k_transpose_narrow<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+        const uint64_t rows_per_tile = G::kItems / a.width / 64 * 64;
+        const uint64_t tiles = (a.rows + rows_per_tile - 1) / rows_per_tile;
+        const uint64_t cap = static_cast<uint64_t>(sms) * occupancy(k_transpose_narrow<T>, 256, smem);
+        k_transpose_narrow<T><<<static_cast<unsigned>(std::min(tiles, cap)), 256, smem, s>>>(a);
     } else {
-        k_transpose<uint32_t><<<grid, block, 0, s>>>(a);
+        // Tile shape sweep (profiles/r01/deinterleave_tiles.jsonl): 128-row
+        // tiles win everywhere; 8-byte items prefer 1 KiB input runs unless
+        // the last tile column would be mostly empty (e.g. W = 129).
+        const uint64_t cover128 = (a.width + 127) / 128 * 128, cover64 = (a.width + 63) / 64 * 64;
+        if (sizeof(T) == 8 && cover128 * 10 <= cover64 * 11)
+            return transpose_wide<T, 128, 1024>(a, sms, s);
+        return transpose_wide<T, 128, 512>(a, sms, s);
     }
     return counted(cudaGetLastError());
+}
+}  // namespace
+
+cudaError_t launch_transpose(const TransposeArgs& a, cudaStream_t s) {
+    if (a.rows == 0 || a.width == 0) return cudaSuccess;
+    return a.itemsize == 8 ? transpose_t<uint64_t>(a, s) : transpose_t<uint32_t>(a, s);
 }
 
 int contig_blocks_per_sm(int fmt, int engine, int block) {

@@ -103,6 +103,26 @@ def test_worker_and_layout_invariance(bcn, cuda, oracle, reference, workers):
             assert np.array_equal(bits(got), bits(serial))
 
 
+@pytest.mark.parametrize("itemsize", [4, 8])
+def test_deinterleave_shapes(bcn, cuda, oracle, itemsize):
+    """Device deinterleave (parallel.cpp:81-97) of arbitrary words against the
+    oracle: narrow (W <= 32, smem row tiles incl. exact tiles W | 8192) and wide
+    (64-row x 512-byte tiles, partial in both directions) regions, ragged
+    Interleaved tails, n smaller than W."""
+    rng = np.random.default_rng(itemsize)
+    dt = np.uint32 if itemsize == 4 else np.uint64
+    for n, w in [(1, 1), (5, 9), (100003, 1), (100003, 5), (100003, 7), (65536, 8), (100003, 31),
+                 (100003, 32), (100003, 33), (100003, 63), (100003, 64), (100003, 65),
+                 (100003, 129), (300007, 1000), (99999, 99999), (2**21 + 17, 4099)]:
+        phys = rng.integers(0, np.iinfo(dt).max, n, dtype=dt, endpoint=True)
+        plan = bcn.par.make_plan(n, w, bcn.Layout.Interleaved)
+        signed = np.int32 if itemsize == 4 else np.int64
+        dev_phys = torch.from_numpy(phys.view(signed)).to(cuda)
+        got = bcn.par.deinterleave(dev_phys, plan).cpu().numpy().view(dt)
+        want = oracle.deinterleave(phys, w)
+        assert np.array_equal(got, want), (n, w)
+
+
 def test_interleaved_ragged_million(bcn, cuda, reference):
     """test_parallel.cpp:98-105: W = 7, n = 10^6, Interleaved."""
     got = dev_fill(bcn, 10**6, O.FMT_F64, workers=7, layout=1)
