@@ -88,10 +88,12 @@ struct DevCtx {
     size_t chunk_bytes = 0;
     unsigned long long* digest = nullptr;
     int* flag = nullptr;
+    void* qscratch = nullptr;         // quality-suite counts / partial sums (grows)
+    size_t qscratch_bytes = 0;
     std::map<int, int> occ;           // (fmt*8+engine) -> blocks per SM
     std::mutex occ_mu;                // guards occ
     std::mutex mu;                    // serialises host-buffer fills on this device
-    std::mutex small_mu;              // serialises users of digest / flag scratch
+    std::mutex small_mu;              // serialises users of digest / flag / qscratch
 };
 
 std::mutex g_ctx_mu;
@@ -119,6 +121,35 @@ bcn_status get_ctx(int device, DevCtx** out) {
         c->init = true;
     }
     *out = c;
+    return BCN_OK;
+}
+
+// Device scratch of at least `bytes` for the quality suite (caller holds small_mu).
+bcn_status quality_scratch(DevCtx* c, size_t bytes, void** out) {
+    if (c->qscratch_bytes < bytes) {
+        if (c->qscratch) BCN_CUDA(cudaFree(c->qscratch));
+        c->qscratch = nullptr;
+        c->qscratch_bytes = 0;
+        BCN_CUDA(cudaMalloc(&c->qscratch, bytes));
+        c->qscratch_bytes = bytes;
+    }
+    *out = c->qscratch;
+    return BCN_OK;
+}
+
+// Stream of a call on device memory. stream != NULL: the caller's stream
+// (ordering against the caller's other work is the caller's business).
+// stream == NULL: the library's internal stream, after every earlier piece of
+// work on the device has finished, so a synchronous call sees all prior
+// writes to its buffers whatever stream made them, like the reference's
+// synchronous functions.
+bcn_status caller_stream(DevCtx* c, void* stream, cudaStream_t* s) {
+    if (stream) {
+        *s = static_cast<cudaStream_t>(stream);
+        return BCN_OK;
+    }
+    BCN_CUDA(cudaDeviceSynchronize());
+    *s = c->stream;
     return BCN_OK;
 }
 
@@ -612,7 +643,7 @@ bcn_status do_fill(void* out, uint64_t capacity, uint64_t n, int fmt, uint32_t w
     j.a_exp = (seed_index - kModulus - 1) % kPeriod;
     j.ctx = c;
     if (kind != PtrKind::Device) return fill_host(j, static_cast<char*>(out), kind == PtrKind::PinnedHost);
-    j.stream = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+    if ((st = caller_stream(c, stream, &j.stream))) return st;
     cudaError_t e = enqueue_range(j, static_cast<char*>(out), 0, plan.n);
     if (e != cudaSuccess) return cuda_fail(e, "fill kernel launch");
     if (!stream) BCN_CUDA(cudaStreamSynchronize(c->stream));
@@ -636,7 +667,7 @@ bcn_status stage_input(const void* buf, size_t bytes, int* device, DeviceInput* 
     if (st) return st;
     if (*device < 0) *device = 0;
     if ((st = get_ctx(*device, ctx))) return st;
-    *s = stream ? static_cast<cudaStream_t>(stream) : (*ctx)->stream;
+    if ((st = caller_stream(*ctx, stream, s))) return st;
     if (kind == PtrKind::Device) {
         in->ptr = buf;
         return BCN_OK;
@@ -852,7 +883,8 @@ bcn_status bcn_deinterleave(const void* in, void* out, uint64_t n, uint32_t work
     if (dev < 0) dev = 0;
     DevCtx* c = nullptr;
     if ((st = get_ctx(dev, &c))) return st;
-    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+    cudaStream_t s;
+    if ((st = caller_stream(c, stream, &s))) return st;
     const void* din = in;
     void* dout = out;
     void* tmp = nullptr;
@@ -905,7 +937,8 @@ bcn_status bcn_seed_states(const uint64_t* a, const uint64_t* k, uint64_t* out, 
     DevCtx* c = nullptr;
     if ((st = get_ctx(dev, &c))) return st;
     std::lock_guard<std::mutex> scratch_lock(c->small_mu);
-    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+    cudaStream_t s;
+    if ((st = caller_stream(c, stream, &s))) return st;
     BCN_CUDA(cudaMemsetAsync(c->flag, 0, sizeof(int), s));
     SeedArgs sa{a, k, out, count, steps, c->flag};
     cudaError_t e = launch_seed(sa, s);
@@ -929,7 +962,8 @@ bcn_status bcn_digest(const void* buf, uint64_t n, uint32_t itemsize, uint64_t i
     DevCtx* c = nullptr;
     if ((st = get_ctx(dev, &c))) return st;
     std::lock_guard<std::mutex> scratch_lock(c->small_mu);
-    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+    cudaStream_t s;
+    if ((st = caller_stream(c, stream, &s))) return st;
     BCN_CUDA(cudaMemsetAsync(c->digest, 0, 3 * sizeof(unsigned long long), s));
     DigestArgs da{buf, n, itemsize, index_base, c->digest};
     if (n) {
@@ -958,7 +992,8 @@ bcn_status constant_writer(const char* what, void* out, uint64_t nbytes, uint64_
     if (kind != PtrKind::Device) return fail(BCN_ERR_INVALID_ARGUMENT, std::string(what) + ": buffer must be device memory");
     DevCtx* c = nullptr;
     if ((st = get_ctx(dev, &c))) return st;
-    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+    cudaStream_t s;
+    if ((st = caller_stream(c, stream, &s))) return st;
     cudaError_t e;
     if (g_pace_gbs.load() > 0.0 || noise_seed) {
         // The Constant writer under the same metering as the paced fill.
@@ -1016,22 +1051,19 @@ bcn_status bcn_chi_square_uniformity(const double* samples, uint64_t n, int bins
     bcn_status st = stage_input(samples, n * sizeof(double), &dev, &in, &c, &s, stream);
     if (st) return st;
     std::lock_guard<std::mutex> scratch_lock(c->small_mu);
-    unsigned long long* counts = nullptr;
-    BCN_CUDA(cudaMalloc(&counts, static_cast<size_t>(bins) * 8));
+    void* scratch = nullptr;
+    if ((st = quality_scratch(c, static_cast<size_t>(bins) * 8, &scratch))) return st;
+    auto* counts = static_cast<unsigned long long*>(scratch);
     BCN_CUDA(cudaMemsetAsync(counts, 0, static_cast<size_t>(bins) * 8, s));
     BCN_CUDA(cudaMemsetAsync(c->flag, 0, sizeof(int), s));
     const int grid = static_cast<int>(std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(c->sms) * 4));
     cudaError_t e = launch_chi_hist(static_cast<const double*>(in.ptr), n, bins, counts, c->flag, grid, s);
-    if (e != cudaSuccess) {
-        cudaFree(counts);
-        return cuda_fail(e, "chi_square launch");
-    }
+    if (e != cudaSuccess) return cuda_fail(e, "chi_square launch");
     std::vector<unsigned long long> h(static_cast<size_t>(bins));
     int flag = 0;
     BCN_CUDA(cudaMemcpyAsync(h.data(), counts, h.size() * 8, cudaMemcpyDeviceToHost, s));
     BCN_CUDA(cudaMemcpyAsync(&flag, c->flag, sizeof(int), cudaMemcpyDeviceToHost, s));
     BCN_CUDA(cudaStreamSynchronize(s));
-    cudaFree(counts);
     if (flag) return fail(BCN_ERR_INVALID_ARGUMENT, "chi_square: sample outside (0,1)");
     double stat = 0.0;
     for (unsigned long long cnt : h) {
@@ -1057,22 +1089,19 @@ bcn_status bcn_monobit_mantissa(const uint64_t* residues, uint64_t n, double* st
     bcn_status st = stage_input(residues, n * 8, &dev, &in, &c, &s, stream);
     if (st) return st;
     std::lock_guard<std::mutex> scratch_lock(c->small_mu);
-    unsigned long long* ones = nullptr;
-    BCN_CUDA(cudaMalloc(&ones, 53 * 8));
+    void* scratch = nullptr;
+    if ((st = quality_scratch(c, 53 * 8, &scratch))) return st;
+    auto* ones = static_cast<unsigned long long*>(scratch);
     BCN_CUDA(cudaMemsetAsync(ones, 0, 53 * 8, s));
     BCN_CUDA(cudaMemsetAsync(c->flag, 0, sizeof(int), s));
     const int grid = static_cast<int>(std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(c->sms) * 4));
     cudaError_t e = launch_monobit(static_cast<const uint64_t*>(in.ptr), n, ones, c->flag, grid, s);
-    if (e != cudaSuccess) {
-        cudaFree(ones);
-        return cuda_fail(e, "monobit launch");
-    }
+    if (e != cudaSuccess) return cuda_fail(e, "monobit launch");
     unsigned long long h[53];
     int flag = 0;
     BCN_CUDA(cudaMemcpyAsync(h, ones, sizeof(h), cudaMemcpyDeviceToHost, s));
     BCN_CUDA(cudaMemcpyAsync(&flag, c->flag, sizeof(int), cudaMemcpyDeviceToHost, s));
     BCN_CUDA(cudaStreamSynchronize(s));
-    cudaFree(ones);
     if (flag) return fail(BCN_ERR_INVALID_ARGUMENT, "monobit: residue out of range");
     const double nn = static_cast<double>(n);
     double worst = 0.0;
@@ -1105,18 +1134,16 @@ bcn_status bcn_serial_correlation(const double* samples, uint64_t n, int lag, do
     if (st) return st;
     const uint64_t pairs = n - static_cast<uint64_t>(lag);
     constexpr int kGrid = 592;  // fixed: the reduction order does not depend on the device
-    double* part = nullptr;
-    BCN_CUDA(cudaMalloc(&part, kGrid * 5 * sizeof(double)));
+    std::lock_guard<std::mutex> scratch_lock(c->small_mu);
+    void* scratch = nullptr;
+    if ((st = quality_scratch(c, kGrid * 5 * sizeof(double), &scratch))) return st;
+    auto* part = static_cast<double*>(scratch);
     cudaError_t e = launch_lag_sums(static_cast<const double*>(in.ptr), pairs, static_cast<uint64_t>(lag), part,
                                     kGrid, s);
-    if (e != cudaSuccess) {
-        cudaFree(part);
-        return cuda_fail(e, "serial_correlation launch");
-    }
+    if (e != cudaSuccess) return cuda_fail(e, "serial_correlation launch");
     std::vector<double> h(kGrid * 5);
     BCN_CUDA(cudaMemcpyAsync(h.data(), part, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
     BCN_CUDA(cudaStreamSynchronize(s));
-    cudaFree(part);
     double sum[5] = {0, 0, 0, 0, 0};
     for (int b = 0; b < kGrid; ++b)
         for (int k = 0; k < 5; ++k) sum[k] += h[b * 5 + k];
