@@ -124,6 +124,28 @@ bcn_status get_ctx(int device, DevCtx** out) {
     return BCN_OK;
 }
 
+// Restores the calling thread's current device on scope exit: entry points
+// switch to the buffer's device (get_ctx) but must not leave the caller's
+// CUDA state (e.g. PyTorch's current device) changed.
+class DeviceGuard {
+  public:
+    DeviceGuard() {
+        if (cudaGetDevice(&prev_) != cudaSuccess) {
+            cudaGetLastError();
+            prev_ = -1;
+        }
+    }
+    ~DeviceGuard() {
+        int now = -1;
+        if (prev_ >= 0 && cudaGetDevice(&now) == cudaSuccess && now != prev_) cudaSetDevice(prev_);
+    }
+    DeviceGuard(const DeviceGuard&) = delete;
+    DeviceGuard& operator=(const DeviceGuard&) = delete;
+
+  private:
+    int prev_ = -1;
+};
+
 // Device scratch of at least `bytes` for the quality suite (caller holds small_mu).
 bcn_status quality_scratch(DevCtx* c, size_t bytes, void** out) {
     if (c->qscratch_bytes < bytes) {
@@ -612,6 +634,7 @@ bcn_status classify(const void* p, int* device, PtrKind* kind) {
 bcn_status do_fill(void* out, uint64_t capacity, uint64_t n, int fmt, uint32_t workers, int layout,
                    uint64_t seed_index, int method, uint64_t base_offset, int engine, int device,
                    void* stream) {
+    DeviceGuard guard;
     Plan plan;
     bcn_status st = make_plan(n, workers, layout, &plan);
     if (st) return st;
@@ -869,6 +892,7 @@ bcn_status bcn_fill_multi(void* const* outs, const int* devices, int ndev, uint6
 
 bcn_status bcn_deinterleave(const void* in, void* out, uint64_t n, uint32_t workers,
                             uint32_t itemsize, int device, void* stream) {
+    DeviceGuard guard;
     Plan p;
     bcn_status st = make_plan(n, workers, 1, &p);
     if (st) return st;
@@ -927,6 +951,7 @@ bcn_status bcn_deinterleave(const void* in, void* out, uint64_t n, uint32_t work
 
 bcn_status bcn_seed_states(const uint64_t* a, const uint64_t* k, uint64_t* out, uint64_t count,
                            uint32_t steps, int device, void* stream) {
+    DeviceGuard guard;
     if (!a || !k || !out) return fail(BCN_ERR_INVALID_ARGUMENT, "seed_states: null buffer");
     if (count == 0) return BCN_OK;
     int dev = device;
@@ -952,6 +977,7 @@ bcn_status bcn_seed_states(const uint64_t* a, const uint64_t* k, uint64_t* out, 
 
 bcn_status bcn_digest(const void* buf, uint64_t n, uint32_t itemsize, uint64_t index_base,
                       uint64_t d[3], int device, void* stream) {
+    DeviceGuard guard;
     if (!buf || !d) return fail(BCN_ERR_INVALID_ARGUMENT, "digest: null buffer");
     if (itemsize != 4 && itemsize != 8) return fail(BCN_ERR_INVALID_ARGUMENT, "digest: itemsize must be 4 or 8");
     int dev = device;
@@ -982,6 +1008,7 @@ namespace {
 // The Constant writer and its noise variant (bcn_fill_constant / bcn_fill_noise).
 bcn_status constant_writer(const char* what, void* out, uint64_t nbytes, uint64_t pattern,
                            uint64_t noise_seed, int device, void* stream) {
+    DeviceGuard guard;
     if (!out) return fail(BCN_ERR_INVALID_ARGUMENT, std::string(what) + ": null buffer");
     if (reinterpret_cast<uintptr_t>(out) % 32 || nbytes % 1024)
         return fail(BCN_ERR_INVALID_ARGUMENT, std::string(what) + ": needs 32-byte alignment and whole 1 KiB rows");
@@ -1037,6 +1064,7 @@ extern "C" {
 
 bcn_status bcn_chi_square_uniformity(const double* samples, uint64_t n, int bins, double* statistic,
                                      int* dof, int* pass, int device, void* stream) {
+    DeviceGuard guard;
     // quality.cpp:21-54 (same preconditions, same formula on exact counts)
     if (!statistic || !dof || !pass) return fail(BCN_ERR_INVALID_ARGUMENT, "chi_square: null output");
     if (n == 0) return fail(BCN_ERR_INVALID_ARGUMENT, "chi_square: no samples");
@@ -1078,6 +1106,7 @@ bcn_status bcn_chi_square_uniformity(const double* samples, uint64_t n, int bins
 
 bcn_status bcn_monobit_mantissa(const uint64_t* residues, uint64_t n, double* statistic, int* worst_bit,
                                 int* pass, int device, void* stream) {
+    DeviceGuard guard;
     // quality.cpp:56-90
     if (!statistic || !worst_bit || !pass) return fail(BCN_ERR_INVALID_ARGUMENT, "monobit: null output");
     if (n < 100000) return fail(BCN_ERR_INVALID_ARGUMENT, "monobit: need at least 1e5 residues");
@@ -1121,6 +1150,7 @@ bcn_status bcn_monobit_mantissa(const uint64_t* residues, uint64_t n, double* st
 
 bcn_status bcn_serial_correlation(const double* samples, uint64_t n, int lag, double* rho, int* pass,
                                   int device, void* stream) {
+    DeviceGuard guard;
     // quality.cpp:92-118; per-block partial sums, fixed-order host reduction.
     if (!rho || !pass) return fail(BCN_ERR_INVALID_ARGUMENT, "serial_correlation: null output");
     if (lag < 1) return fail(BCN_ERR_INVALID_ARGUMENT, "serial_correlation: lag must be positive");
