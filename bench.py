@@ -364,8 +364,20 @@ def main() -> None:
             B.par.fill_format(host, hplan, A0, B.Method.BarrettModified, start, fmt, engine=engine)
         dt = sharding.max_over_ranks(time.perf_counter() - t0, coll_dev)
         barrier()
+        # The e2e roofline: a plain D2H copy of the same bytes into the same
+        # pinned buffer (PCIe bound), timed the same way.
+        src = buf[:count]
+        host.copy_(src)
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            host.copy_(src)
+        torch.cuda.synchronize(dev)
+        d2h_gbs = count * isz * args.e2e_steps / (time.perf_counter() - t0) / 1e9
+        e2e_gbs = count * isz * args.e2e_steps / dt / 1e9
         e2e = {"value": total_items * args.e2e_steps / dt, "unit": UNIT, "h2d_bytes_per_step": 0,
                "d2h_bytes_per_step": count * isz, "steps": args.e2e_steps,
+               "gbs_delivered": e2e_gbs, "d2h_copy_gbs": d2h_gbs, "frac_of_d2h_copy": e2e_gbs / d2h_gbs,
                "note": "bcn_fill with a pinned host pointer: chunked device generation + D2H on "
                        "two streams; inputs are scalar kernel arguments (seed index, offset, "
                        "count), so there is no H2D buffer"}

@@ -204,13 +204,19 @@ std::atomic<int> g_pace_formats{(1 << kFmtU64) | (1 << kFmtF64)};
 
 // CTAs of the paced grid: ctas_per_sm x SMs, or BCN_PACE_GRID (an
 // exploration override: total CTAs, e.g. to leave SMs idle under a power cap).
-uint64_t paced_grid(const DevCtx* c) {
+// The interleaved kernel does ~20 instructions per variate against ~15 for the
+// contiguous one and needs more worker warps per SM to keep up with the pacer
+// (profiles/r01/interleaved_cps.jsonl, TB/s with 1 / 2 / 3 CTAs per SM:
+// W = 7: 5.0 / 5.6 / 6.3; W = 64...100003: 5.2-5.5 / 5.8-6.0 / 5.7-5.9).
+uint64_t paced_grid(const DevCtx* c, uint64_t interleaved_width = 0) {
     static const long env = [] {
         const char* v = std::getenv("BCN_PACE_GRID");
         return v ? std::strtol(v, nullptr, 10) : 0L;
     }();
     if (env > 0) return static_cast<uint64_t>(env);
-    return static_cast<uint64_t>(c->sms) * g_pace_cps.load();
+    int cps = g_pace_cps.load();
+    if (interleaved_width) cps = std::max(interleaved_width <= 32 ? 3 : 2, cps);
+    return static_cast<uint64_t>(c->sms) * cps;
 }
 
 // Per-CTA phase offset of the pacing schedule (BCN_PACE_STAGGER=0|1,
@@ -389,7 +395,7 @@ cudaError_t enqueue_region(const FillJob& j, char* dptr, uint64_t slot0, uint64_
         if (g_pace_gbs.load() > 0.0 && (g_pace_formats.load() >> j.fmt & 1)) {
             // Paced, grid-strided: each stream advances nwk rows = S slots per round.
             constexpr uint64_t kWorkers = kPacedThreads / 32 - 1;
-            const uint64_t want = paced_grid(j.ctx);
+            const uint64_t want = paced_grid(j.ctx, width);
             const int grid = static_cast<int>(std::max<uint64_t>(1, std::min(want, (rows + kWorkers - 1) / kWorkers)));
             const unsigned __int128 S =
                 static_cast<unsigned __int128>(row) * grid * kWorkers * paced_rows_per_round(j.fmt);

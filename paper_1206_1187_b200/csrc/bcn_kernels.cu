@@ -265,6 +265,16 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
     const uint32_t rounds =
         a.rows > first ? static_cast<uint32_t>((a.rows - first + per_round - 1) / per_round) : 0;
     if (rounds == 0) return;  // uniform across the CTA
+    // Interleaved: the two jump multipliers in shared memory, so a stream picks
+    // its multiplier with one indexed (broadcast) load instead of selects.
+    __shared__ Mult jumps[2];
+    if constexpr (INTER) {
+        if (threadIdx.x == 0) {
+            jumps[0] = a.jump;
+            jumps[1] = a.jump_wrap;
+        }
+        __syncthreads();
+    }
     if (warp == kWorkers) {
         // Pacer: release round k no earlier than t0 + k * gap (one timer read
         // and one CTA barrier per round). With `stagger`, each CTA's t0 is
@@ -295,7 +305,13 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
     // rows this worker owns: w, w+nwk, ... (< a.rows)
     const uint32_t count = a.rows > w ? static_cast<uint32_t>((a.rows - w + nwk - 1) / nwk) : 0;
     typename E::State st[H][V];
-    uint64_t col[INTER ? H : 1][INTER ? V : 1];  // interleaved: worker index of each stream's slot
+    // interleaved: worker index of each stream's slot (< width < 2^32). A
+    // stream stays in the same physical row iff col < same_below; col then
+    // advances by adv_b, otherwise by adv_b - width (mod 2^32).
+    uint32_t col[INTER ? H : 1][INTER ? V : 1];
+    const uint32_t same_below = static_cast<uint32_t>(a.width - a.adv_b);
+    const uint32_t adv_same = static_cast<uint32_t>(a.adv_b);
+    const uint32_t adv_wrap = static_cast<uint32_t>(a.adv_b - a.width);
     // Constant writer pattern: a.e0 everywhere, or (a.q0 != 0, exploration)
     // fixed per-thread random words, to separate data-toggling power from
     // generator power.
@@ -320,7 +336,7 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
 #pragma unroll
                 for (int v = 0; v < V; ++v) {
                     const uint64_t q = a.q0 + row * ROW + lane * V + v;
-                    col[h][v] = q % a.width;
+                    col[h][v] = static_cast<uint32_t>(q % a.width);
                     const uint64_t j = col[h][v] * a.wpw + a.i_base + q / a.width;
                     st[h][v] = E::from_canonical(dev_state_from_exp(dev_exp_at(a.e0, j)));
                 }
@@ -364,9 +380,9 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
             for (int h = 0; h < H; ++h)
 #pragma unroll
                 for (int v = 0; v < V; ++v) {
-                    const bool same = col[h][v] + a.adv_b < a.width;
-                    st[h][v] = E::mul(st[h][v], same ? k : a.jump_wrap);
-                    col[h][v] = same ? col[h][v] + a.adv_b : col[h][v] + a.adv_b - a.width;
+                    const bool same = col[h][v] < same_below;
+                    st[h][v] = E::mul(st[h][v], jumps[same ? 0 : 1]);
+                    col[h][v] += same ? adv_same : adv_wrap;
                 }
         } else if constexpr (!CONST) {
 #pragma unroll
@@ -392,11 +408,14 @@ __global__ void __launch_bounds__(kContigThreads) k_fill_interleaved(const Inter
     if (r >= r_end) return;
 
     typename E::State st[V];
-    uint64_t col[V];  // worker index of each stream's current slot
+    uint32_t col[V];  // worker index of each stream's current slot (see k_fill_paced)
+    const uint32_t same_below = static_cast<uint32_t>(a.width - a.adv_b);
+    const uint32_t adv_same = static_cast<uint32_t>(a.adv_b);
+    const uint32_t adv_wrap = static_cast<uint32_t>(a.adv_b - a.width);
 #pragma unroll
     for (int v = 0; v < V; ++v) {
         const uint64_t q = a.q0 + r * ROW + lane * V + v;
-        col[v] = q % a.width;
+        col[v] = static_cast<uint32_t>(q % a.width);
         const uint64_t j = col[v] * a.wpw + a.i_base + q / a.width;
         st[v] = E::from_canonical(dev_state_from_exp(dev_exp_at(a.e0, j)));
     }
@@ -409,9 +428,9 @@ __global__ void __launch_bounds__(kContigThreads) k_fill_interleaved(const Inter
         pack_store<FMT>(p, bits);
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-            const bool same = col[v] + a.adv_b < a.width;
+            const bool same = col[v] < same_below;
             st[v] = E::mul(st[v], same ? a.jump_same : a.jump_wrap);
-            col[v] = same ? col[v] + a.adv_b : col[v] + a.adv_b - a.width;
+            col[v] += same ? adv_same : adv_wrap;
         }
         p += kRowBytes;
     }

@@ -78,12 +78,12 @@ inline uint64_t host_jump(uint64_t steps_mod_p) { return host_pow2(host_mul53_mo
 // Every engine consumes the same packed multiplier so kernels can be engine
 // generic: c (canonical), its Shoup constant, its Montgomery image, and the
 // FP64 pair (balanced value, RN(balanced/m)).
-struct Mult {
+struct alignas(16) Mult {
+    double cb;    // balanced multiplier (FP64 engine); cb, com first: one 16-byte load
+    double com;   // RN(cb / m)
     uint64_t c;
     uint64_t shoup;
     uint64_t mont;
-    double cb;
-    double com;
     int64_t cbi;  // balanced multiplier as an integer (mixed engine)
 };
 
