@@ -181,7 +181,7 @@ ENGINE_NAMES = {"auto": "Auto", "barrett": "Barrett", "montgomery": "Montgomery"
 
 def kernel_name(fmt: int, engine: int, paced: bool) -> str:
     """Template instance name of the dominant kernel for (format, engine)."""
-    if paced and fmt != 2 and engine in (1, 2, 3):
+    if paced and fmt != 2 and engine in (3, 6):  # FP64-pipe engines are paced
         return f"void k_fill_paced<{fmt}, {engine}, 0>(PacedArgs)"
     if engine == 4:
         return f"void k_fill_staged<{fmt}>(StagedArgs)"

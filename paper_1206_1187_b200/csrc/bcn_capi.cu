@@ -212,7 +212,9 @@ std::atomic<int> g_pace_formats{(1 << kFmtU64) | (1 << kFmtF64)};
 // contiguous one and needs more worker warps per SM to keep up with the pacer
 // (profiles/r01/interleaved_cps.jsonl, TB/s with 1 / 2 / 3 CTAs per SM:
 // W = 7: 5.0 / 5.6 / 6.3; W = 64...100003: 5.2-5.5 / 5.8-6.0 / 5.7-5.9).
-uint64_t paced_grid(const DevCtx* c, uint64_t interleaved_width = 0) {
+// The Mixed engine (~1 DFMA + 8 integer ops per step) likewise needs 2 CTAs
+// per SM (profiles/r01/tune_engines_cps.jsonl: 5.8 TB/s with 1, 7.05 with 2).
+uint64_t paced_grid(const DevCtx* c, int engine, uint64_t interleaved_width = 0) {
     static const long env = [] {
         const char* v = std::getenv("BCN_PACE_GRID");
         return v ? std::strtol(v, nullptr, 10) : 0L;
@@ -220,7 +222,18 @@ uint64_t paced_grid(const DevCtx* c, uint64_t interleaved_width = 0) {
     if (env > 0) return static_cast<uint64_t>(env);
     int cps = g_pace_cps.load();
     if (interleaved_width) cps = std::max(interleaved_width <= 32 ? 3 : 2, cps);
+    if (engine == kEngMixed) cps = std::max(2, cps);
     return static_cast<uint64_t>(c->sms) * cps;
+}
+
+// Pacing only helps a kernel that can outrun the write path. The integer
+// engines (Barrett ~26, Montgomery ~30 instructions per variate) are
+// compute-bound below it and run faster unpaced at full occupancy (paced at
+// 1..4 CTAs per SM: Barrett 3.9-5.6 TB/s, Montgomery 3.3-4.5,
+// tune_engines_cps.jsonl; unpaced: 6.1 / 4.8, ab_f64.jsonl).
+bool paced(int fmt, int engine) {
+    return g_pace_gbs.load() > 0.0 && (g_pace_formats.load() >> fmt & 1) &&
+           (engine == kEngFP64 || engine == kEngMixed);
 }
 
 // Per-CTA phase offset of the pacing schedule (BCN_PACE_STAGGER=0|1,
@@ -331,11 +344,11 @@ cudaError_t enqueue_affine(const FillJob& j, char* dptr, uint64_t slot0, uint64_
             const uint64_t persistent = static_cast<uint64_t>(j.ctx->sms) * bulk_blocks_per_sm(j.fmt);
             const int grid = static_cast<int>(std::max<uint64_t>(1, std::min(persistent, tiles)));
             e = launch_bulk(j.fmt, c, grid, j.stream);
-        } else if (g_pace_gbs.load() > 0.0 && (g_pace_formats.load() >> j.fmt & 1)) {
+        } else if (paced(j.fmt, j.engine)) {
             // Paced path (by default for the 8-byte formats; f32 with the
             // FP64 engine is FP64-pipe bound below the write roof).
             constexpr uint64_t kWorkers = kPacedThreads / 32 - 1;
-            const uint64_t want = paced_grid(j.ctx);
+            const uint64_t want = paced_grid(j.ctx, j.engine);
             const int grid = static_cast<int>(std::max<uint64_t>(1, std::min(want, (rows + kWorkers - 1) / kWorkers)));
             PacedArgs pa{};
             pa.out = c.out;
@@ -396,10 +409,10 @@ cudaError_t enqueue_region(const FillJob& j, char* dptr, uint64_t slot0, uint64_
         r.jump_wrap = mult_for_steps((static_cast<__int128>(r.adv_b) - static_cast<__int128>(width)) *
                                          static_cast<__int128>(p.wpw) +
                                      adv_a + 1);
-        if (g_pace_gbs.load() > 0.0 && (g_pace_formats.load() >> j.fmt & 1)) {
+        if (paced(j.fmt, engine)) {
             // Paced, grid-strided: each stream advances nwk rows = S slots per round.
             constexpr uint64_t kWorkers = kPacedThreads / 32 - 1;
-            const uint64_t want = paced_grid(j.ctx, width);
+            const uint64_t want = paced_grid(j.ctx, engine, width);
             const int grid = static_cast<int>(std::max<uint64_t>(1, std::min(want, (rows + kWorkers - 1) / kWorkers)));
             const unsigned __int128 S =
                 static_cast<unsigned __int128>(row) * grid * kWorkers * paced_rows_per_round(j.fmt);

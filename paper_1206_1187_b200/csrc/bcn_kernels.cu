@@ -955,9 +955,9 @@ cudaError_t launch_contig(int fmt, int engine, const ContigArgs& a, int grid, in
 namespace {
 template <int FMT, int MODE>
 cudaError_t paced_mode(int engine, const PacedArgs& a, int grid, cudaStream_t s) {
+    // Only the FP64-pipe engines are paced (bcn_capi.cu: paced()); the integer
+    // engines are compute-bound below the write path and run unpaced.
     switch (engine) {
-        case kEngBarrett: k_fill_paced<FMT, kEngBarrett, MODE><<<grid, kPacedThreads, 0, s>>>(a); break;
-        case kEngMontgomery: k_fill_paced<FMT, kEngMontgomery, MODE><<<grid, kPacedThreads, 0, s>>>(a); break;
         case kEngFP64: k_fill_paced<FMT, kEngFP64, MODE><<<grid, kPacedThreads, 0, s>>>(a); break;
         case kEngMixed: k_fill_paced<FMT, kEngMixed, MODE><<<grid, kPacedThreads, 0, s>>>(a); break;
         default: return cudaErrorInvalidValue;
