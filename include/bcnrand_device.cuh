@@ -14,11 +14,27 @@
 // is to_unit_interval(next()) (generator.hpp:74-78); state_at(a, k) equals
 // gen::state_at (generator.cpp:42-49), computed from the closed form
 // z_k = m - 2^((a - 3^33 - 1 + 53 k) mod P) mod m with a square-and-multiply
-// over exact 128-bit products (no tables, no host set-up). Seeds out of range
-// are the caller's responsibility (validate on the host with bcn_seed_from_index).
+// over exact products reduced by a 128-bit Barrett step (no tables, no host
+// set-up, no 128-bit division). Seeds out of range are the caller's
+// responsibility (validate on the host with bcn_seed_from_index).
+//
+// The header also compiles as plain C++ (host only), which is how the CPU
+// test suite checks its arithmetic (tests/cpp/test_device_api_host.cpp).
 #pragma once
 
 #include <cstdint>
+
+#if !defined(__CUDACC__)
+#ifndef __host__
+#define __host__
+#endif
+#ifndef __device__
+#define __device__
+#endif
+#ifndef __forceinline__
+#define __forceinline__ inline
+#endif
+#endif
 
 namespace bcn {
 namespace dev {
@@ -29,8 +45,27 @@ constexpr uint64_t kMu = 0x33D9481681D79Dull;       // floor(2^106 / m)
 constexpr uint64_t kMinSeedIndex = kModulus + 100;
 constexpr uint64_t kMaxSeedIndex = 1ull << 53;
 
+__host__ __device__ __forceinline__ uint64_t umulhi(uint64_t a, uint64_t b) {
+#if defined(__CUDA_ARCH__)
+    return __umul64hi(a, b);
+#else
+    return static_cast<uint64_t>((static_cast<unsigned __int128>(a) * b) >> 64);
+#endif
+}
+
+// a b mod m for a, b < m by a Barrett step on the 105-bit product x = a b:
+// q = floor(floor(x / 2^51) mu / 2^55) with mu = floor(2^106 / m). Writing
+// x = x1 2^51 + x0 and mu = 2^106/m - d (0 <= d < 1),
+//     x/m - x1 mu / 2^55 = x0/m + x1 d / 2^55 < 2^51/m + 2^53.6/2^55 < 0.8,
+// so q is floor(x/m) or one less, r = x - q m lies in [0, 2m) (exact mod
+// 2^64) and one conditional subtract finishes. ~20 integer instructions
+// instead of a software 128-bit division.
 __host__ __device__ __forceinline__ uint64_t mulmod(uint64_t a, uint64_t b) {
-    return static_cast<uint64_t>(static_cast<unsigned __int128>(a) * b % kModulus);
+    const uint64_t lo = a * b, hi = umulhi(a, b);
+    const uint64_t x1 = (hi << 13) | (lo >> 51);  // floor(x / 2^51) < 2^54
+    const uint64_t q = (umulhi(x1, kMu) << 9) | ((x1 * kMu) >> 55);
+    const uint64_t r = lo - q * kModulus;
+    return r >= kModulus ? r - kModulus : r;
 }
 
 // 2^e mod m by square-and-multiply (generator.cpp:17-30 restated).
@@ -47,11 +82,7 @@ __host__ __device__ inline uint64_t pow2(uint64_t e) {
 
 // The paper's modified Barrett step z -> 2^53 z mod m, valid on [1, m).
 __host__ __device__ __forceinline__ uint64_t step(uint64_t z) {
-#if defined(__CUDA_ARCH__)
-    const uint64_t hi = __umul64hi(z, kMu);
-#else
-    const uint64_t hi = static_cast<uint64_t>((static_cast<unsigned __int128>(z) * kMu) >> 64);
-#endif
+    const uint64_t hi = umulhi(z, kMu);
     const uint64_t lo = z * kMu;
     const uint64_t q3 = (hi << 11) | (lo >> 53);
     const uint64_t r = 0x20000000000000ull - ((q3 * kModulus) & 0x1FFFFFFFFFFFFFull);

@@ -20,6 +20,18 @@ REFTESTS = os.path.join(ROOT, "oracle", "_ref", "ref_tests_on_b200")
 DEVICE_API = os.path.join(ROOT, "tests", "cpp", "build", "test_device_api")
 
 
+def test_device_api_arithmetic_on_host():
+    """include/bcnrand_device.cuh compiled as plain C++: the Barrett mulmod
+    against exact 128-bit arithmetic (edges + 2e7 random pairs), the step,
+    skip-ahead composition and the reference goldens — no GPU involved."""
+    r = subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp"), "device_host"],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([os.path.join(ROOT, "tests", "cpp", "build", "test_device_api_host")],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "[device-api-host] ok" in r.stdout, r.stdout + r.stderr
+
+
 def test_dropin_headers_compile_and_link(bcn):
     """Builds against the headers + product library here (no GPU needed)."""
     r = subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp"), "dropin"],
