@@ -236,16 +236,6 @@ bool paced(int fmt, int engine) {
            (engine == kEngFP64 || engine == kEngMixed);
 }
 
-// Per-CTA phase offset of the pacing schedule (BCN_PACE_STAGGER=0|1,
-// exploration knob; default 0).
-int pace_stagger() {
-    static const int env = [] {
-        const char* v = std::getenv("BCN_PACE_STAGGER");
-        return v ? static_cast<int>(std::strtol(v, nullptr, 10)) : 0;
-    }();
-    return env;
-}
-
 uint64_t pace_gap_q8(int grid, double gbs, int fmt, bool constant = false) {
     // One round of the grid writes grid * 8 workers * H rows * 1 KiB;
     // 1 GB/s == 1 byte/ns.
@@ -356,7 +346,6 @@ cudaError_t enqueue_affine(const FillJob& j, char* dptr, uint64_t slot0, uint64_
             pa.e0 = c.e0;
             pa.jump = mult_for_steps(static_cast<__int128>(row) * grid * kWorkers * paced_rows_per_round(j.fmt));
             pa.gap_q8 = pace_gap_q8(grid, g_pace_gbs.load(), j.fmt);
-            pa.stagger = pace_stagger();
             pa.mode = kPacedContiguous;
             e = launch_paced(j.fmt, j.engine, pa, grid, j.stream);
         } else {
@@ -422,7 +411,6 @@ cudaError_t enqueue_region(const FillJob& j, char* dptr, uint64_t slot0, uint64_
             pa.rows = rows;
             pa.e0 = r.e0;
             pa.gap_q8 = pace_gap_q8(grid, g_pace_gbs.load(), j.fmt);
-            pa.stagger = pace_stagger();
             pa.mode = kPacedInterleaved;
             pa.q0 = r.q0;
             pa.width = width;
@@ -1103,7 +1091,6 @@ bcn_status constant_writer(const char* what, void* out, uint64_t nbytes, uint64_
         pa.rows = rows;
         pa.e0 = pattern;
         pa.gap_q8 = g_pace_gbs.load() > 0.0 ? pace_gap_q8(grid, g_pace_gbs.load(), kFmtU64, true) : 0;
-        pa.stagger = pace_stagger();
         pa.mode = kPacedConstant;
         pa.q0 = noise_seed;  // != 0: per-thread pseudo-random words instead of `pattern`
         e = launch_paced(kFmtU64, -1, pa, grid, s);

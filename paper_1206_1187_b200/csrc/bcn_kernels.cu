@@ -277,15 +277,11 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
     }
     if (warp == kWorkers) {
         // Pacer: release round k no earlier than t0 + k * gap (one timer read
-        // and one CTA barrier per round). With `stagger`, each CTA's t0 is
-        // shifted by a golden-ratio fraction of a round so the grid's bursts
-        // are spread over the round instead of leaving together.
+        // and one CTA barrier per round; staggering the CTAs' schedules or
+        // releasing each worker separately measured no better,
+        // profiles/r01/timeline_stagger.jsonl).
         uint64_t t0 = 0;
-        if (lane == 0) {
-            t0 = global_ns();
-            if (a.stagger)
-                t0 += (a.gap_q8 * ((blockIdx.x * 2654435761u) >> 24)) >> 16;
-        }
+        if (lane == 0) t0 = global_ns();
         for (uint32_t k = 0; k < rounds; ++k) {
             if (lane == 0 && a.gap_q8) {
                 const uint64_t target = t0 + ((static_cast<uint64_t>(k) * a.gap_q8) >> 8);

@@ -42,7 +42,6 @@ struct PacedArgs {
     uint64_t e0;      // exponent of element 0 (or the 8-byte pattern, Constant)
     Mult jump;        // per round: contiguous 2^(53 * H * nwk * ROW); interleaved: same-row advance
     uint64_t gap_q8;  // ns between CTA rounds, x256 (0 = unpaced)
-    int stagger;      // 1: per-CTA phase offset of the pacing schedule; 0: none
     int mode;         // PacedMode (interleaved uses the fields below, as InterleavedArgs)
     uint64_t q0, width, i_base, wpw, adv_b;
     Mult jump_wrap;

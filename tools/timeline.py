@@ -99,7 +99,7 @@ def main() -> None:
     load = [s for s in samples if t0 <= s[0] <= t1]
     print(json.dumps({
         "tag": a.tag, "fmt": a.fmt, "engine": a.engine, "pace": a.pace, "cps": a.cps,
-        "stagger": os.environ.get("BCN_PACE_STAGGER", "0"), "launches": a.launches,
+        "launches": a.launches,
         "gbs_all": round(nbytes * a.launches / (sum(per) * 1e-3) / 1e9, 1),
         "gbs_first": round(nbytes / (per[0] * 1e-3) / 1e9, 1),
         "gbs_buckets": buckets,
