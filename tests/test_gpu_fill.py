@@ -140,6 +140,32 @@ def test_interleaved_engines_formats(bcn, cuda, oracle, engine, fmt):
 
 
 # ----------------------------------------------------- offsets and wraps
+@pytest.mark.parametrize("engine", ["FP64", "Barrett"])
+def test_f32_is_rz_of_f64_full_size(bcn, cuda, engine):
+    """f32 := RZ(to_unit_interval(z)) over 2^30 variates: the f32
+    fill equals the truncation of the (oracle-verified) f64 fill element by
+    element (a size-independent property; the count of variates within 3 ulps
+    of a truncation boundary is printed)."""
+    n = 1 << 30
+    plan = bcn.par.make_plan(n, 1)
+    f64 = torch.empty(n, dtype=torch.float64, device=cuda)
+    f32 = torch.empty(n, dtype=torch.float32, device=cuda)
+    bcn.par.fill_format(f64, plan, A0, bcn.Method.BarrettModified, 0, bcn.Format.F64, engine=bcn.Engine.FP64)
+    bcn.par.fill_format(f32, plan, A0, bcn.Method.BarrettModified, 0, bcn.Format.F32,
+                        engine=bcn.Engine[engine])
+    torch.cuda.synchronize()
+    near = 0
+    step = 1 << 26
+    for c in range(0, n, step):
+        b = f64[c:c + step].view(torch.int64)
+        want = ((b >> 29) - (896 << 23)) & 0xFFFFFFFF
+        got = f32[c:c + step].view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+        assert torch.equal(got, want), f"chunk at {c}"
+        low = b & ((1 << 29) - 1)
+        near += int((((low + 3) & ((1 << 29) - 1)) < 7).logical_and(f64[c:c + step] > 0.5).sum())
+    print(f"boundary re-check candidates in 2^30: {near}")
+
+
 def test_base_offset_windows(bcn, cuda, oracle):
     """test_parallel.cpp:131-138 and test_cli.cpp:116-125 (chunked == single)."""
     whole = dev_fill(bcn, 1 << 20, O.FMT_U64)
