@@ -279,7 +279,14 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
         // Pacer: release round k no earlier than t0 + k * gap (one timer read
         // and one CTA barrier per round; staggering the CTAs' schedules or
         // releasing each worker separately measured no better,
-        // profiles/r01/timeline_stagger.jsonl).
+        // profiles/r01/timeline_stagger.jsonl). Pacer and workers meet at
+        // named barrier 1 from different bar.sync instructions — the
+        // warp-specialised producer/consumer pattern of CUTLASS's
+        // NamedBarrier. compute-sanitizer synccheck reports it as divergence
+        // (tools/c/barrier_probe.cu reproduces that on a 20-line kernel);
+        // the alternatives it accepts measured slower: non-aligned
+        // barrier.sync -3.5%, one shared bar.sync instruction -9%
+        // (profiles/r01/ab_barrier.jsonl). memcheck / racecheck are clean.
         uint64_t t0 = 0;
         if (lane == 0) t0 = global_ns();
         for (uint32_t k = 0; k < rounds; ++k) {
