@@ -297,6 +297,7 @@ cudaError_t enqueue_slots(const FillJob& j, char* dptr, uint64_t slot0, uint64_t
 cudaError_t enqueue_affine(const FillJob& j, char* dptr, uint64_t slot0, uint64_t count,
                            uint64_t e_first) {
     const int isz = format_itemsize(j.fmt);
+    if (count == 0) return cudaSuccess;
     const uint64_t addr = reinterpret_cast<uint64_t>(dptr);
     if (j.engine == kEngStaged) {
         const uint64_t tile = static_cast<uint64_t>(kStagedThreads) * kStagedL;
@@ -318,23 +319,32 @@ cudaError_t enqueue_affine(const FillJob& j, char* dptr, uint64_t slot0, uint64_
         return enqueue_slots(j, dptr + done * isz, slot0 + done, count - done);
     }
     const uint64_t row = 32ull * (32 / isz);
-    const uint64_t head = std::min<uint64_t>(count, ((32 - addr % 32) % 32) / isz);
-    const uint64_t rows = (count - head) / row;
-    cudaError_t e = enqueue_slots(j, dptr, slot0, head);
-    if (e != cudaSuccess) return e;
-    if (rows) {
-        ContigArgs c;
-        c.out = dptr + head * isz;
+    if (j.engine != kEngBulk) {
+        // Whole rows from the 32-byte aligned address at or below dptr; the
+        // partial first / last rows are written by the same kernel
+        // (EdgeRow), so a range is exactly one launch.
+        const uint64_t lo = (addr % 32) / isz;  // elements of the first row before dptr
+        char* base = dptr - lo * isz;
+        EdgeRow edge[2] = {};
+        uint64_t consumed = 0;
+        if (lo) {
+            consumed = std::min<uint64_t>(count, row - lo);
+            edge[0] = EdgeRow{base, exp_add(e_first, kPeriod - lo), static_cast<uint32_t>(lo),
+                              static_cast<uint32_t>(lo + consumed)};
+            base += row * isz;
+        }
+        const uint64_t rows = (count - consumed) / row;
+        const uint64_t tail = (count - consumed) % row;
+        if (tail)
+            edge[1] = EdgeRow{base + rows * row * isz, exp_add(e_first, consumed + rows * row), 0,
+                              static_cast<uint32_t>(tail)};
+        ContigArgs c{};
+        c.out = base;
         c.rows = rows;
-        c.e0 = exp_add(e_first, head);
-        if (j.engine == kEngBulk) {
-            // Streams advance one 16-row tile per step (k_fill_bulk).
-            c.jump_row = mult_for_steps(static_cast<__int128>(row) * kBulkTileRows);
-            const uint64_t tiles = (rows + kBulkTileRows - 1) / kBulkTileRows;
-            const uint64_t persistent = static_cast<uint64_t>(j.ctx->sms) * bulk_blocks_per_sm(j.fmt);
-            const int grid = static_cast<int>(std::max<uint64_t>(1, std::min(persistent, tiles)));
-            e = launch_bulk(j.fmt, c, grid, j.stream);
-        } else if (paced(j.fmt, j.engine)) {
+        c.e0 = exp_add(e_first, consumed);
+        c.edge[0] = edge[0];
+        c.edge[1] = edge[1];
+        if (paced(j.fmt, j.engine)) {
             // Paced path (by default for the 8-byte formats; f32 with the
             // FP64 engine is FP64-pipe bound below the write roof).
             constexpr uint64_t kWorkers = kPacedThreads / 32 - 1;
@@ -347,13 +357,32 @@ cudaError_t enqueue_affine(const FillJob& j, char* dptr, uint64_t slot0, uint64_
             pa.jump = mult_for_steps(static_cast<__int128>(row) * grid * kWorkers * paced_rows_per_round(j.fmt));
             pa.gap_q8 = pace_gap_q8(grid, g_pace_gbs.load(), j.fmt);
             pa.mode = kPacedContiguous;
-            e = launch_paced(j.fmt, j.engine, pa, grid, j.stream);
-        } else {
-            const int grid = grid_for_rows(j.ctx, j.fmt, j.engine, false, rows);
-            c.stride_order = static_cast<uint32_t>(g_row_order.load());
-            const uint64_t step_rows = c.stride_order ? static_cast<uint64_t>(grid) * (kContigThreads / 32) : 1;
-            c.jump_row = mult_for_steps(static_cast<__int128>(row) * step_rows);
-            e = launch_contig(j.fmt, j.engine, c, grid, kContigThreads, j.stream);
+            pa.edge[0] = edge[0];
+            pa.edge[1] = edge[1];
+            return launch_paced(j.fmt, j.engine, pa, grid, j.stream);
+        }
+        const int grid = grid_for_rows(j.ctx, j.fmt, j.engine, false, std::max<uint64_t>(rows, 1));
+        c.stride_order = static_cast<uint32_t>(g_row_order.load());
+        const uint64_t step_rows = c.stride_order ? static_cast<uint64_t>(grid) * (kContigThreads / 32) : 1;
+        c.jump_row = mult_for_steps(static_cast<__int128>(row) * step_rows);
+        return launch_contig(j.fmt, j.engine, c, grid, kContigThreads, j.stream);
+    }
+    const uint64_t head = std::min<uint64_t>(count, ((32 - addr % 32) % 32) / isz);
+    const uint64_t rows = (count - head) / row;
+    cudaError_t e = enqueue_slots(j, dptr, slot0, head);
+    if (e != cudaSuccess) return e;
+    if (rows) {
+        ContigArgs c{};
+        c.out = dptr + head * isz;
+        c.rows = rows;
+        c.e0 = exp_add(e_first, head);
+        {
+            // Streams advance one 16-row tile per step (k_fill_bulk).
+            c.jump_row = mult_for_steps(static_cast<__int128>(row) * kBulkTileRows);
+            const uint64_t tiles = (rows + kBulkTileRows - 1) / kBulkTileRows;
+            const uint64_t persistent = static_cast<uint64_t>(j.ctx->sms) * bulk_blocks_per_sm(j.fmt);
+            const int grid = static_cast<int>(std::max<uint64_t>(1, std::min(persistent, tiles)));
+            e = launch_bulk(j.fmt, c, grid, j.stream);
         }
         if (e != cudaSuccess) return e;
     }

@@ -170,6 +170,48 @@ __device__ __forceinline__ void pack_store(void* p, const uint64_t (&bits)[Fmt<F
     st256(p, w);
 }
 
+// One partial row (EdgeRow), written by a whole warp: each lane seeds its V
+// elements (one windowed power + T=1 steps), converts them with the canonical
+// path (bit-identical to every engine) and stores the in-range ones.
+template <int FMT>
+__device__ __forceinline__ void fill_edge_row(const EdgeRow& er, unsigned lane) {
+    constexpr int V = Fmt<FMT>::kVec;
+    using Item = typename Fmt<FMT>::Item;
+    const uint32_t t0 = lane * V;
+    uint64_t z = dev_state_from_exp(dev_exp_at(er.e0, t0));
+    uint64_t bits[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+        if constexpr (FMT == kFmtU64)
+            bits[v] = z;
+        else if constexpr (FMT == kFmtF64)
+            bits[v] = static_cast<uint64_t>(__double_as_longlong(unit_from_u64(z)));
+        else
+            bits[v] = __float_as_uint(f32_rz_from_unit(unit_from_u64(z)));
+        if (v + 1 < V) z = step_modified_barrett(z);
+    }
+    char* p = static_cast<char*>(er.base) + t0 * sizeof(Item);
+    if (t0 >= er.lo && t0 + V <= er.hi) {
+        pack_store<FMT>(p, bits);
+    } else {
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+            if (t0 + v >= er.lo && t0 + v < er.hi) {
+                if constexpr (sizeof(Item) == 8)
+                    reinterpret_cast<uint64_t*>(p)[v] = bits[v];
+                else
+                    reinterpret_cast<uint32_t*>(p)[v] = static_cast<uint32_t>(bits[v]);
+            }
+    }
+}
+
+// Warps 0 and 1 of CTA 0 write the head / tail edge rows, if any.
+template <int FMT>
+__device__ __forceinline__ void fill_edges(const EdgeRow (&edge)[2]) {
+    const unsigned warp = threadIdx.x >> 5;
+    if (blockIdx.x == 0 && warp < 2 && edge[warp].base) fill_edge_row<FMT>(edge[warp], threadIdx.x & 31);
+}
+
 // Splits `rows` over `nw` warps: warp w gets [begin, end).
 __device__ __forceinline__ void warp_rows(uint64_t rows, uint64_t nw, uint64_t w, uint64_t& begin,
                                           uint64_t& end) {
@@ -203,6 +245,7 @@ __global__ void __launch_bounds__(kContigThreads) k_fill_contig(const ContigArgs
         warp_rows(a.rows, nw, w, r, r_end);
         step = 1;
     }
+    fill_edges<FMT>(a.edge);
     if (r >= r_end) return;
 
     // Seed: one windowed power per lane, then T=1 steps for the lane's vector.
@@ -264,6 +307,7 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
     const uint64_t per_round = H * nwk;
     const uint32_t rounds =
         a.rows > first ? static_cast<uint32_t>((a.rows - first + per_round - 1) / per_round) : 0;
+    if constexpr (!CONST && !INTER) fill_edges<FMT>(a.edge);
     if (rounds == 0) return;  // uniform across the CTA
     // Interleaved: the two jump multipliers in shared memory, so a stream picks
     // its multiplier with one indexed (broadcast) load instead of selects.

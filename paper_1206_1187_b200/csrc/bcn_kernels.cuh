@@ -23,6 +23,16 @@ enum Engine : int {
 
 inline int format_itemsize(int fmt) { return fmt == kFmtF32 ? 4 : 8; }
 
+// A partial row at either end of a contiguous range, written inside the main
+// kernel (by warps 0 / 1 of CTA 0) instead of by extra launches: the row
+// starts at the 32-byte aligned `base`, its element t has 2-exponent
+// (e0 + 53 t) mod P, and only elements t in [lo, hi) are stored.
+struct EdgeRow {
+    void* base;  // nullptr: no edge row
+    uint64_t e0;
+    uint32_t lo, hi;
+};
+
 // Contiguous fast path: `rows` full rows of 32 lanes x 32 bytes starting at the
 // 32-byte aligned `out`; element j of `out` has 2-exponent (e0 + 53 j) mod P.
 struct ContigArgs {
@@ -31,6 +41,7 @@ struct ContigArgs {
     uint64_t e0;
     Mult jump_row;          // 2^(53 * elements per stream step) mod m
     uint32_t stride_order;  // 0: per-warp row ranges; 1: grid-strided rows
+    EdgeRow edge[2];        // partial head / tail rows (or none)
 };
 
 // Paced contiguous fill (k_fill_paced): grid-strided rows metered to a
@@ -45,6 +56,7 @@ struct PacedArgs {
     int mode;         // PacedMode (interleaved uses the fields below, as InterleavedArgs)
     uint64_t q0, width, i_base, wpw, adv_b;
     Mult jump_wrap;
+    EdgeRow edge[2];  // contiguous mode: partial head / tail rows (or none)
 };
 
 // Interleaved region fast path (reference Layout::Interleaved,
