@@ -39,8 +39,15 @@ constexpr double kMagic = 6755399441055744.0;         // 1.5 * 2^52
 constexpr int kPowWindows = 13;  // 13 x 4-bit windows cover E < P < 2^52
 
 // ---------------------------------------------------------------- host exact
+// a b mod m for a, b < m: a 128-bit Barrett step instead of a 128-bit
+// division (q = floor(floor(ab / 2^51) mu / 2^55) is floor(ab/m) or one less;
+// proof and CPU test with include/bcnrand_device.cuh's identical mulmod).
 inline uint64_t host_mulmod(uint64_t a, uint64_t b) {
-    return static_cast<uint64_t>(static_cast<unsigned __int128>(a) * b % kModulus);
+    const unsigned __int128 x = static_cast<unsigned __int128>(a) * b;
+    const uint64_t x1 = static_cast<uint64_t>(x >> 51);
+    const uint64_t q = static_cast<uint64_t>((static_cast<unsigned __int128>(x1) * kMu) >> 55);
+    const uint64_t r = static_cast<uint64_t>(x) - q * kModulus;
+    return r >= kModulus ? r - kModulus : r;
 }
 inline uint64_t host_pow2(uint64_t e) {  // 2^e mod m, e reduced mod P first
     e %= kPeriod;
