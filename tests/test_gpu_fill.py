@@ -326,6 +326,53 @@ def test_fill_noise_writer(bcn, cuda):
         bcn.device.fill_noise(c, seed=0)
 
 
+def test_concurrent_calls_from_threads(bcn, cuda, oracle):
+    """The C ABI is re-entrant like the reference (parallel.cpp has no global
+    state): eight host threads mixing device fills on their own streams, host
+    (pageable / pinned) fills, digests and quality calls all get the right bits."""
+    import threading
+
+    n = 300007
+    want = {fmt: oracle.fill(n, fmt, base_offset=99) for fmt in (O.FMT_U64, O.FMT_F64, O.FMT_F32)}
+    errors = []
+
+    def worker(t):
+        try:
+            fmt = (O.FMT_U64, O.FMT_F64, O.FMT_F32)[t % 3]
+            plan = bcn.par.make_plan(n, 1 + t % 4)
+            for it in range(3):
+                if (t + it) % 3 == 0:
+                    s = torch.cuda.Stream(device=cuda)
+                    dt = {O.FMT_U64: torch.int64, O.FMT_F64: torch.float64, O.FMT_F32: torch.float32}[fmt]
+                    buf = torch.empty(n, dtype=dt, device=cuda)
+                    with torch.cuda.stream(s):
+                        bcn.par.fill_format(buf, plan, A0, bcn.Method.BarrettModified, 99,
+                                            bcn.Format(fmt), stream=s)
+                    s.synchronize()
+                    got = buf.cpu().numpy()
+                    bcn.device.digest(buf.view(torch.int32 if fmt == O.FMT_F32 else torch.int64))
+                elif (t + it) % 3 == 1:
+                    got = np.empty(n, dtype=want[fmt].dtype)
+                    bcn.par.fill_format(got, plan, A0, bcn.Method.BarrettModified, 99, bcn.Format(fmt))
+                else:
+                    got = torch.empty(n, dtype={O.FMT_U64: torch.int64, O.FMT_F64: torch.float64,
+                                                O.FMT_F32: torch.float32}[fmt], pin_memory=True)
+                    bcn.par.fill_format(got, plan, A0, bcn.Method.BarrettModified, 99, bcn.Format(fmt))
+                    got = got.numpy()
+                    bcn.quality.serial_correlation(torch.from_numpy(oracle.fill(200000, O.FMT_F64)).to(cuda))
+                if not np.array_equal(bits(got), bits(want[fmt])):
+                    errors.append((t, it, fmt))
+        except Exception as e:  # noqa: BLE001
+            errors.append((t, repr(e)))
+
+    threads = [threading.Thread(target=worker, args=(t,)) for t in range(8)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors
+
+
 def test_fill_multi_concatenation(bcn, cuda, oracle):
     """make_plan(n, G) contiguous shards (one per 'device'; two shards on GPU 0
     here) concatenate to the single fill."""
