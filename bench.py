@@ -190,9 +190,12 @@ def kernel_name(fmt: int, engine: int, paced: bool) -> str:
     return f"void k_fill_contig<{fmt}, {engine}>(ContigArgs)"
 
 
-def ncu_traffic(kernel: str) -> tuple[float | None, str | None]:
-    """dram read+write bytes per launch of `kernel` from the newest committed
-    `ncu --set full` summary under profiles/ (tools/ncu_summary.py)."""
+def ncu_traffic(kernel: str, algorithmic_bytes: float) -> tuple[float | None, str | None]:
+    """dram read+write bytes per launch of `kernel` from the committed
+    `ncu --set full` summaries under profiles/ (tools/ncu_summary.py): of the
+    captured launches of that kernel, the one whose size matches this launch
+    (traffic closest to its algorithmic bytes; the capture also holds smaller
+    launches of the same kernel)."""
     import glob
 
     best = None
@@ -204,8 +207,10 @@ def ncu_traffic(kernel: str) -> tuple[float | None, str | None]:
             continue
         for r in rows if isinstance(rows, list) else []:
             if r.get("kernel", "").strip() == kernel and "traffic_bytes" in r:
-                best = (r["traffic_bytes"], os.path.relpath(path, ROOT))
-    return best if best else (None, None)
+                d = abs(r["traffic_bytes"] - algorithmic_bytes)
+                if best is None or d < best[0]:
+                    best = (d, r["traffic_bytes"], os.path.relpath(path, ROOT))
+    return (best[1], best[2]) if best else (None, None)
 
 
 def main() -> None:
@@ -398,8 +403,8 @@ def main() -> None:
     if rank == 0:
         pace = lib.bcn_write_pacing()
         kname = kernel_name(int(fmt), int(resolved), pace > 0)
-        traffic, traffic_src = ncu_traffic(kname)
         bytes_per_launch = count * isz / launches_per_step
+        traffic, traffic_src = ncu_traffic(kname, bytes_per_launch)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,

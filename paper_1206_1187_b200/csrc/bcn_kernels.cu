@@ -720,18 +720,40 @@ __global__ void __launch_bounds__(256) k_seed(const SeedArgs a) {
 }
 
 // ------------------------------------------------------------- digest
+// 8 loads in flight per thread per pass (unguarded when the pass is whole);
+// the sums are order-independent mod 2^64, so the result does not depend on
+// the grid.
+template <typename T>
+__device__ __forceinline__ void digest_t(const DigestArgs& a, unsigned long long& s, unsigned long long& ws,
+                                         unsigned long long& x) {
+    constexpr int U = 8;
+    const T* buf = static_cast<const T*>(a.buf);
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i0 < a.n; i0 += U * stride) {
+        uint64_t v[U];
+        if (i0 + (U - 1) * stride < a.n) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) v[u] = buf[i0 + u * stride];
+        } else {
+#pragma unroll
+            for (int u = 0; u < U; ++u) v[u] = i0 + u * stride < a.n ? buf[i0 + u * stride] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t g = i0 + u * stride + a.index_base;
+            s += v[u];
+            ws += (g + 1) * v[u];
+            x ^= v[u] * (2 * g + 1);
+        }
+    }
+}
+
 __global__ void __launch_bounds__(256) k_digest(const DigestArgs a) {
     unsigned long long s = 0, ws = 0, x = 0;
-    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < a.n;
-         i += stride) {
-        const uint64_t v = a.itemsize == 8 ? static_cast<const uint64_t*>(a.buf)[i]
-                                           : static_cast<const uint32_t*>(a.buf)[i];
-        const uint64_t g = i + a.index_base;
-        s += v;
-        ws += (g + 1) * v;
-        x ^= v * (2 * g + 1);
-    }
+    if (a.itemsize == 8)
+        digest_t<uint64_t>(a, s, ws, x);
+    else
+        digest_t<uint32_t>(a, s, ws, x);
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
         s += __shfl_xor_sync(0xffffffffu, s, o);
