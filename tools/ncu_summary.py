@@ -85,9 +85,17 @@ def summarise_launches(path: str) -> dict:
         if len(r) > vi and r[mi] == "gpu__time_duration.sum":
             agg[r[ki]].append(float(r[vi].replace(",", "")))
     tot = sum(sum(v) for v in agg.values())
-    return {"source": path.split("/")[-1], "unit": "ns", "kernels": {
-        k: {"launches": len(v), "sum_ns": sum(v), "mean_ns": sum(v) / len(v), "share": sum(v) / tot}
-        for k, v in agg.items()}}
+
+    def entry(v):
+        # A kernel may run at several sizes in one command (e.g. the bench's
+        # full-size fills and its 64 MiB host-output chunks): `large` holds
+        # the launches within 2x of the longest one.
+        big = [x for x in v if x >= 0.5 * max(v)]
+        return {"launches": len(v), "sum_ns": sum(v), "mean_ns": sum(v) / len(v), "share": sum(v) / tot,
+                "large": {"launches": len(big), "mean_ns": sum(big) / len(big), "min_ns": min(big),
+                          "max_ns": max(big)}}
+
+    return {"source": path.split("/")[-1], "unit": "ns", "kernels": {k: entry(v) for k, v in agg.items()}}
 
 
 def main() -> None:
