@@ -1,19 +1,29 @@
 // bcn_kernels.cu — sm_100a kernels for the alpha_{2,3} generator fill path.
 //
 // Kernel inventory:
-//   k_fill_contig<FMT, ENG>       logical-order fill, lane-interleaved jump streams,
-//                                 256-bit stores (STG.E.256), persistent grid.
-//   k_fill_interleaved<FMT, ENG>  reference Layout::Interleaved, same machinery
-//                                 with a per-stream row-crossing multiplier select.
+//   k_fill_paced<FMT, ENG, MODE>  the default 8-byte fill: grid-strided 1 KiB rows,
+//                                 8 worker warps + 1 pacer warp per CTA metering the
+//                                 stores to a target HBM write rate; MODE selects the
+//                                 contiguous layout, the reference Layout::Interleaved,
+//                                 or the Constant / noise writer.
+//   k_fill_contig<FMT, ENG>       unpaced logical-order fill (f32, integer engines),
+//                                 lane-interleaved jump streams, 256-bit stores,
+//                                 persistent grid. Both contiguous kernels write the
+//                                 partial first / last rows themselves (EdgeRow).
+//   k_fill_interleaved<FMT, ENG>  unpaced Layout::Interleaved (per-stream row-crossing
+//                                 multiplier).
+//   k_fill_bulk<FMT, ENG>         FP64 jump streams staged in smem, TMA bulk stores.
 //   k_fill_staged<FMT>            the paper's T=1 modified-Barrett step per thread,
 //                                 tile staged in smem, TMA bulk store per tile.
-//   k_fill_slots<FMT>             exact per-slot reference semantics (head/tail,
-//                                 u64-wrap corner cases); one seed per slot.
+//   k_fill_slots<FMT>             exact per-slot reference semantics (interleaved
+//                                 heads/tails, u64-wrap corner cases); one seed per slot.
 //   k_seed                        batched state_at / next walks (skip-ahead stress).
 //   k_digest                      order-sensitive checksums for verification.
-//   k_constant                    the Constant writer: identical access pattern,
-//                                 fixed value (the paper's memory ceiling).
-//   k_transpose                   device deinterleave (Interleaved -> logical).
+//   k_constant                    the unpaced Constant writer: identical access
+//                                 pattern, fixed value (the paper's memory ceiling).
+//   k_transpose, k_transpose_narrow
+//                                 device deinterleave (Interleaved -> logical),
+//                                 pipelined shared-memory tiles.
 #include <cuda_runtime.h>
 
 #include <cstdint>
