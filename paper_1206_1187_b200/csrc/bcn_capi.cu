@@ -18,6 +18,7 @@
 #include <functional>
 #include <map>
 #include <mutex>
+#include <numeric>
 #include <string>
 #include <thread>
 #include <vector>
@@ -427,9 +428,41 @@ cudaError_t enqueue_region(const FillJob& j, char* dptr, uint64_t slot0, uint64_
         r.jump_wrap = mult_for_steps((static_cast<__int128>(r.adv_b) - static_cast<__int128>(width)) *
                                          static_cast<__int128>(p.wpw) +
                                      adv_a + 1);
-        if (paced(j.fmt, engine)) {
+        constexpr uint64_t kWorkers = kPacedThreads / 32 - 1;
+        // Column-stable paced grid: a round advances every stream by
+        // S = row * kWorkers * H * grid slots; when width divides S the stream
+        // stays in its worker column and steps by one multiplier (S / width
+        // elements), as in the contiguous kernel. The grid must then be a
+        // multiple of width / gcd(width, row * kWorkers * H): taken if such a
+        // grid keeps >= 95% of the contiguous grid (W = 7: 147 CTAs, W = 64:
+        // 148) or >= 80% of a 2-CTA-per-SM grid (W = 1000: 250);
+        // profiles/r01/interleaved_fixed*.jsonl.
+        const uint64_t per_cta = row * kWorkers * paced_rows_per_round(j.fmt);
+        const uint64_t unit = width / std::gcd(width, per_cta);
+        const uint64_t need = std::max<uint64_t>(1, (rows + kWorkers - 1) / kWorkers);
+        auto fixed_for = [&](uint64_t base, uint64_t pct) -> uint64_t {
+            base = std::min(base, need);
+            const uint64_t g = base / unit * unit;
+            return g >= 1 && g * 100 >= base * pct ? g : 0;
+        };
+        uint64_t fixed_grid = fixed_for(paced_grid(j.ctx, engine), 95);
+        if (!fixed_grid) fixed_grid = fixed_for(2ull * j.ctx->sms, 80);
+        if (paced(j.fmt, engine) && fixed_grid) {
+            const uint64_t S = per_cta * fixed_grid;
+            PacedArgs pa{};
+            pa.out = r.out;
+            pa.rows = rows;
+            pa.e0 = r.e0;
+            pa.gap_q8 = pace_gap_q8(static_cast<int>(fixed_grid), g_pace_gbs.load(), j.fmt);
+            pa.mode = kPacedInterleavedFixed;
+            pa.q0 = r.q0;
+            pa.width = width;
+            pa.i_base = i_base;
+            pa.wpw = p.wpw;
+            pa.jump = mult_for_steps(static_cast<__int128>(S / width));
+            e = launch_paced(j.fmt, engine, pa, static_cast<int>(fixed_grid), j.stream);
+        } else if (paced(j.fmt, engine)) {
             // Paced, grid-strided: each stream advances nwk rows = S slots per round.
-            constexpr uint64_t kWorkers = kPacedThreads / 32 - 1;
             const uint64_t want = paced_grid(j.ctx, engine, width);
             const int grid = static_cast<int>(std::max<uint64_t>(1, std::min(want, (rows + kWorkers - 1) / kWorkers)));
             const unsigned __int128 S =

@@ -305,7 +305,8 @@ template <int FMT, int ENG, int MODE>
 __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a) {
     using E = Eng<ENG>;
     constexpr bool CONST = MODE == kPacedConstant;
-    constexpr bool INTER = MODE == kPacedInterleaved;
+    constexpr bool INTER = MODE == kPacedInterleaved;  // per-stream row-crossing multiplier
+    constexpr bool INTER_SEED = INTER || MODE == kPacedInterleavedFixed;
     constexpr int V = Fmt<FMT>::kVec;
     constexpr int H = paced_rows_per_round(FMT, CONST);  // rows per worker per round
     constexpr uint64_t ROW = 32ull * V;
@@ -317,7 +318,7 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
     const uint64_t per_round = H * nwk;
     const uint32_t rounds =
         a.rows > first ? static_cast<uint32_t>((a.rows - first + per_round - 1) / per_round) : 0;
-    if constexpr (!CONST && !INTER) fill_edges<FMT>(a.edge);
+    if constexpr (!CONST && !INTER_SEED) fill_edges<FMT>(a.edge);
     if (rounds == 0) return;  // uniform across the CTA
     // Interleaved: the two jump multipliers in shared memory, so a stream picks
     // its multiplier with one indexed (broadcast) load instead of selects.
@@ -389,12 +390,13 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
 #pragma unroll
         for (int h = 0; h < H; ++h) {
             const uint64_t row = w + h * nwk;
-            if constexpr (INTER) {
+            if constexpr (INTER_SEED) {
 #pragma unroll
                 for (int v = 0; v < V; ++v) {
                     const uint64_t q = a.q0 + row * ROW + lane * V + v;
-                    col[h][v] = static_cast<uint32_t>(q % a.width);
-                    const uint64_t j = col[h][v] * a.wpw + a.i_base + q / a.width;
+                    const uint64_t c = q % a.width;
+                    if constexpr (INTER) col[h][v] = static_cast<uint32_t>(c);
+                    const uint64_t j = c * a.wpw + a.i_base + q / a.width;
                     st[h][v] = E::from_canonical(dev_state_from_exp(dev_exp_at(a.e0, j)));
                 }
             } else {
@@ -1050,8 +1052,11 @@ cudaError_t paced_fmt(int engine, const PacedArgs& a, int grid, cudaStream_t s) 
         k_fill_paced<FMT, kEngBarrett, kPacedConstant><<<grid, kPacedThreads, 0, s>>>(a);
         return counted(cudaGetLastError());
     }
-    return a.mode == kPacedInterleaved ? paced_mode<FMT, kPacedInterleaved>(engine, a, grid, s)
-                                       : paced_mode<FMT, kPacedContiguous>(engine, a, grid, s);
+    switch (a.mode) {
+        case kPacedInterleaved: return paced_mode<FMT, kPacedInterleaved>(engine, a, grid, s);
+        case kPacedInterleavedFixed: return paced_mode<FMT, kPacedInterleavedFixed>(engine, a, grid, s);
+        default: return paced_mode<FMT, kPacedContiguous>(engine, a, grid, s);
+    }
 }
 }  // namespace
 

@@ -46,7 +46,10 @@ struct ContigArgs {
 
 // Paced contiguous fill (k_fill_paced): grid-strided rows metered to a
 // target HBM write rate by one pacer warp per CTA.
-enum PacedMode : int { kPacedContiguous = 0, kPacedConstant = 1, kPacedInterleaved = 2 };
+// kPacedInterleavedFixed: an interleaved region whose per-round slot advance
+// is a multiple of the width, so every stream stays in its worker column and
+// steps by ONE multiplier (the contiguous kernel's stepping, interleaved seeding).
+enum PacedMode : int { kPacedContiguous = 0, kPacedConstant = 1, kPacedInterleaved = 2, kPacedInterleavedFixed = 3 };
 struct PacedArgs {
     void* out;        // 32-byte aligned
     uint64_t rows;    // rows of 32 lanes x 32 bytes
