@@ -689,9 +689,10 @@ __global__ void __launch_bounds__(kContigThreads) k_fill_bulk(const ContigArgs a
 // SeedArgs.steps == 0: out[t] = state_at(a[t], k[t]) (generator.cpp:42-49).
 // steps > 0: out[t*steps + s] = the (s+1)-th next() from that state.
 __global__ void __launch_bounds__(256) k_seed(const SeedArgs a) {
-    // Walk outputs are staged 8 steps at a time in shared memory ([thread][8],
-    // padded) so the block writes each thread's 64-byte pieces with 8 lanes
-    // per piece instead of one 8-byte store per lane per step.
+    // Walk outputs: 32-byte vector stores per thread when steps % 4 == 0 and
+    // the output is 32-byte aligned; otherwise staged 8 steps at a time in
+    // shared memory ([thread][8], padded) so the block writes each thread's
+    // 64-byte pieces with 8 lanes per piece.
     constexpr int kChunk = 8;
     __shared__ uint64_t stage[256][kChunk + 1];
     const uint64_t t0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x;
@@ -711,6 +712,20 @@ __global__ void __launch_bounds__(256) k_seed(const SeedArgs a) {
     }
     if (a.steps == 0) {
         if (live) a.out[t] = z;
+        return;
+    }
+    if (a.steps % 4 == 0 && reinterpret_cast<uintptr_t>(a.out) % 32 == 0) {
+        // Each thread's walk is one contiguous run of steps * 8 bytes: write it
+        // with 32-byte vector stores (every store fills whole sectors; L2
+        // assembles the lines), no staging or cross-thread validity lookups.
+        if (!live) return;
+        uint64_t* dst = a.out + t * a.steps;
+        for (uint32_t s = 0; s < a.steps; s += 4) {
+            uint64_t v[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) v[i] = z = step_modified_barrett(z);
+            st256(dst + s, v);
+        }
         return;
     }
     const uint64_t nthreads = a.count - t0 < blockDim.x ? a.count - t0 : blockDim.x;

@@ -286,6 +286,9 @@ def test_seed_states_stress(bcn, cuda, oracle):
     sub = 1 << 14
     walks = bcn.device.seed_states(ta[:sub], tk[:sub], steps=64).cpu().numpy().view(np.uint64)
     assert np.array_equal(walks, oracle.seed_batch(a[:sub], k[:sub], steps=64))
+    for steps in (1, 3, 12):  # staged (steps % 4 != 0) and vector-store walk paths
+        walks = bcn.device.seed_states(ta[:999], tk[:999], steps=steps).cpu().numpy().view(np.uint64)
+        assert np.array_equal(walks, oracle.seed_batch(a[:999], k[:999], steps=steps))
     bad = ta[:4].clone()
     bad[2] = A0 - 1
     with pytest.raises(bcn.OutOfRange):
