@@ -396,6 +396,10 @@ def main() -> None:
         cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
                "sample": f"reference par::fill (oracle/_ref = unmodified /root/reference sources, "
                          f"g++ -O3) of 2^27 doubles, W={threads} threads, {secs:.2f} s"}
+        # the single-thread rate too (config 1 = 10^6 doubles).
+        rate1, secs1 = reference_rate(10**6, 1, reps=5)
+        cpu["single_thread"] = {"value": rate1, "unit": UNIT, "cores": 1,
+                                "sample": f"config 1: par::fill of 10^6 doubles, W=1, {secs1 * 1e3:.1f} ms"}
 
     ab_rows = run_ab(B, torch, dev, stream, timed, buf, fmt, args.ab) if args.ab else []
     sweep_rows = run_sweep(B, dev, stream, timed) if args.sweep else []
