@@ -376,6 +376,27 @@ def test_concurrent_calls_from_threads(bcn, cuda, oracle):
     assert not errors, errors
 
 
+def test_fill_inside_cuda_graph(bcn, cuda, oracle):
+    """bcn_fill on a caller stream is a plain kernel launch, so it can be
+    captured in a CUDA graph and replayed (launch-bound loops of small fills)."""
+    n = 100003
+    outs = [torch.empty(n, dtype=torch.float64, device=cuda) for _ in range(3)]
+    plan = bcn.par.make_plan(n, 1)
+    s = torch.cuda.Stream(device=cuda)
+    bcn.par.fill(outs[0], plan, A0, stream=s)  # warm-up: device context, occupancy caches
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for i, o in enumerate(outs):
+            bcn.par.fill(o, plan, A0, base_offset=i * n, stream=torch.cuda.current_stream())
+    for o in outs:
+        o.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    for i, o in enumerate(outs):
+        assert np.array_equal(bits(o.cpu().numpy()), bits(oracle.fill(n, O.FMT_F64, base_offset=i * n)))
+
+
 def test_fill_multi_concatenation(bcn, cuda, oracle):
     """make_plan(n, G) contiguous shards (one per 'device'; two shards on GPU 0
     here) concatenate to the single fill."""
