@@ -242,6 +242,21 @@ def test_host_numpy_output_chunked(bcn, cuda, oracle):
                                                                       workers=3)))
 
 
+@pytest.mark.parametrize("workers", [7, 1000])
+def test_host_output_interleaved_across_chunks(bcn, cuda, oracle, workers):
+    """Interleaved layout into host memory: the 64 MiB device chunks cut the
+    interleaved regions at arbitrary slots (pageable and pinned outputs)."""
+    n = (1 << 24) + 12345
+    plan = bcn.par.make_plan(n, workers, bcn.Layout.Interleaved)
+    want = oracle.fill(n, O.FMT_F64, base_offset=5, workers=workers, layout=1)
+    out = np.empty(n, dtype=np.float64)
+    bcn.par.fill(out, plan, A0, base_offset=5)
+    assert np.array_equal(bits(out), bits(want))
+    pinned = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    bcn.par.fill(pinned, plan, A0, base_offset=5)
+    assert np.array_equal(bits(pinned.numpy()), bits(want))
+
+
 def test_host_pinned_output(bcn, cuda, oracle):
     n = (1 << 23) + 3
     out = torch.empty(n, dtype=torch.float32, pin_memory=True)
