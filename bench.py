@@ -50,6 +50,8 @@ def parse() -> argparse.Namespace:
     p.add_argument("--fmt", default="f64", choices=["f64", "u64", "f32"])
     p.add_argument("--engine", default="auto")
     p.add_argument("--log2n", type=int, default=30)
+    p.add_argument("--pace", type=float, default=None,
+                   help="override the library's write-pacing target (GB/s; 0 = unpaced)")
     p.add_argument("--e2e-steps", type=int, default=5)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
@@ -248,6 +250,9 @@ def main() -> None:
         if world > 1:
             dist.barrier()
 
+    if args.pace is not None:
+        _, cps, mask = B.device.write_pacing_config()
+        B.device.set_write_pacing(args.pace, cps, mask)
     fmt = B.Format[args.fmt.upper()]
     engine = B.Engine[ENGINE_NAMES[args.engine]]
     resolved = B.Engine(_lib.lib().bcn_auto_engine(int(fmt))) if engine == B.Engine.Auto else engine
