@@ -166,6 +166,32 @@ def test_f32_is_rz_of_f64_full_size(bcn, cuda, engine):
     print(f"boundary re-check candidates in 2^30: {near}")
 
 
+def test_randomized_plans_against_oracle(bcn, cuda, oracle):
+    """Seeded fuzz over the whole fill surface: random n (incl. < one row),
+    workers, layout, format, engine, pointer misalignment, seed index and
+    base_offset (incl. near 2^64 and near multiples of the period) — every
+    case bit-exact against the oracle. Exercises the in-kernel edge rows,
+    the column-stable and two-multiplier interleaved paths and the slot kernel."""
+    rng = np.random.default_rng(0x1206_1187)
+    P = 3706040377703682
+    engines = ["Auto", "Barrett", "Montgomery", "FP64", "Staged", "Bulk", "Mixed"]
+    for case in range(400):
+        n = int(rng.choice([rng.integers(1, 300), rng.integers(300, 5000), rng.integers(5000, 400000)]))
+        workers = int(rng.choice([1, 2, 3, 5, 7, 8, 16, 31, 33, 64, 100, 1000, rng.integers(1, 5000)]))
+        layout = int(rng.integers(0, 2))
+        fmt = int(rng.choice([O.FMT_U64, O.FMT_F64, O.FMT_F32]))
+        engine = str(rng.choice(engines))
+        offset = int(rng.integers(0, 9))
+        seed = int(rng.choice([A0, 1 << 53, rng.integers(A0, (1 << 53) + 1)]))
+        base = int(rng.choice([0, rng.integers(0, 1 << 62), (1 << 64) - int(rng.integers(1, 2 * n + 2)),
+                               P * int(rng.integers(1, 1000)) - int(rng.integers(0, n + 1))]))
+        base &= (1 << 64) - 1
+        got = dev_fill(bcn, n, fmt, workers=workers, layout=layout, seed=seed, base=base,
+                       engine=engine, offset=offset)
+        want = oracle.fill(n, fmt, seed_index=seed, base_offset=base, workers=workers, layout=layout)
+        assert np.array_equal(bits(got), bits(want)), (case, n, workers, layout, fmt, engine, offset, seed, base)
+
+
 def test_base_offset_windows(bcn, cuda, oracle):
     """test_parallel.cpp:131-138 and test_cli.cpp:116-125 (chunked == single)."""
     whole = dev_fill(bcn, 1 << 20, O.FMT_U64)
