@@ -40,8 +40,10 @@ def main() -> None:
         ("paced f64 Barrett", lambda: fill(f64, B.Format.F64, B.Engine.Barrett)),
         ("bulk f64", lambda: fill(f64, B.Format.F64, B.Engine.Bulk)),
         ("staged f64 (paper T=1 + TMA)", lambda: fill(f64, B.Format.F64, B.Engine.Staged)),
-        ("paced interleaved W=7", lambda: fill(f64, B.Format.F64,
-                                               p=B.par.make_plan(n, 7, B.Layout.Interleaved))),
+        ("paced interleaved W=7 (column-stable)", lambda: fill(f64, B.Format.F64,
+                                                               p=B.par.make_plan(n, 7, B.Layout.Interleaved))),
+        ("paced interleaved W=100003 (two multipliers)",
+         lambda: fill(f64, B.Format.F64, p=B.par.make_plan(n, 100003, B.Layout.Interleaved))),
         ("paced constant", lambda: B.device.fill_constant(u64)),
         ("paced noise writer", lambda: B.device.fill_noise(u64)),
     ]
