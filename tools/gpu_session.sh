@@ -1,7 +1,4 @@
 # Scratch driver for one gpurun call (edited per experiment).
 set -x
-timeout 300 python bench.py > gpurun_out/bench_default.json 2>>gpurun_out/err.log
-timeout 300 python bench.py --impl reference > gpurun_out/bench_reference_arm.json 2>>gpurun_out/err.log
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_bench.csv python bench.py --steps 20 --warmup 3 --no-cpu > gpurun_out/bench_under_ncu.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -o /tmp/prof_all python tools/profile_all.py > gpurun_out/prof_all.log 2>&1
-python tools/ncu_summary.py /tmp/prof_all.ncu-rep -o gpurun_out/ncu_full_all_kernels.json >> gpurun_out/prof_all.log 2>&1
+timeout 600 python tools/inter_perf.py --workers 7,125,250,500,1000,1024,1536,2000 --cps 1 --rounds 2 > gpurun_out/inter.jsonl 2>>gpurun_out/err.log
+timeout 600 ncu --metrics gpu__time_duration.sum,launch__grid_size --clock-control none -k regex:k_fill_paced --csv --log-file gpurun_out/inter_launches.csv python tools/inter_perf.py --workers 7,1000,1024 --cps 1 --rounds 1 > /dev/null 2>&1

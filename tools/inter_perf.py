@@ -19,14 +19,21 @@ import paper_1206_1187_b200 as B  # noqa: E402
 
 
 def main() -> None:
+    import argparse
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workers", default="1,7,64,1000,100003")
+    ap.add_argument("--cps", default="1,2,3")
+    ap.add_argument("--rounds", type=int, default=2)
+    args = ap.parse_args()
     dev = torch.device("cuda:0")
     stream = torch.cuda.current_stream(dev)
     n = 1 << 30
     buf = torch.empty(n, dtype=torch.float64, device=dev)
-    for rnd in range(2):
-        for w in (1, 7, 64, 1000, 100003):
+    for rnd in range(args.rounds):
+        for w in [int(x) for x in args.workers.split(",")]:
             plan = B.par.make_plan(n, w, B.Layout.Interleaved)
-            for cps in (1, 2, 3):
+            for cps in [int(x) for x in args.cps.split(",")]:
                 B.device.set_write_pacing(7200, cps, 3)
                 fn = lambda: B.par.fill(buf, plan, B.kMinSeedIndex, stream=stream)  # noqa: E731
                 fn()
