@@ -75,6 +75,7 @@ class ClockSampler:
 
     def __init__(self, index: int):
         self.samples: list[int] = []
+        self.power: list[float] = []
         self.reasons = 0
         self.max_mhz = None
         self._stop = threading.Event()
@@ -95,6 +96,7 @@ class ClockSampler:
             try:
                 self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
                 self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.power.append(nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
             except Exception:  # noqa: BLE001
                 pass
             time.sleep(0.005)
@@ -112,8 +114,15 @@ class ClockSampler:
 
     def summary(self) -> dict:
         names = [v for k, v in self.REASONS.items() if self.reasons & k and k != 0x1]
+        limit = None
+        try:
+            limit = self.nvml.nvmlDeviceGetEnforcedPowerLimit(self.h) / 1000.0 if self.nvml else None
+        except Exception:  # noqa: BLE001
+            pass
         return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
-                "sm_max_mhz": self.max_mhz, "samples": len(self.samples), "reasons": names}
+                "sm_max_mhz": self.max_mhz, "samples": len(self.samples), "reasons": names,
+                "power_w_median": statistics.median(self.power) if self.power else None,
+                "power_limit_w": limit}
 
 
 # ------------------------------------------------------------ reference arm
