@@ -96,7 +96,10 @@ class ClockSampler:
             try:
                 self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
                 self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                self.power.append(nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
+                # instantaneous reading: the default power usage is a ~1 s average
+                v = nv.nvmlDeviceGetFieldValues(self.h, [nv.NVML_FI_DEV_POWER_INSTANT])[0]
+                if v.nvmlReturn == 0:
+                    self.power.append(v.value.uiVal / 1000.0)
             except Exception:  # noqa: BLE001
                 pass
             time.sleep(0.005)
@@ -121,7 +124,7 @@ class ClockSampler:
             pass
         return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
                 "sm_max_mhz": self.max_mhz, "samples": len(self.samples), "reasons": names,
-                "power_w_median": statistics.median(self.power) if self.power else None,
+                "power_w_median": statistics.median(self.power) if self.power else None,  # instantaneous
                 "power_limit_w": limit}
 
 

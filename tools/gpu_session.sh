@@ -1,4 +1,5 @@
 # Scratch driver for one gpurun call (edited per experiment).
 set -x
-timeout 900 python -m pytest tests -m gpu -x -q -k quality 2>&1 | tail -2 > gpurun_out/pytest_gpu.log
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_monobit --csv --log-file gpurun_out/mono_launches.csv python tools/quality_perf.py > gpurun_out/qp.log 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3 > gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
+timeout 300 python bench.py > gpurun_out/bench_default.json 2>>gpurun_out/err.log
