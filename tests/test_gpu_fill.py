@@ -25,7 +25,11 @@ def dev_fill(bcn, n, fmt=O.FMT_F64, *, workers=1, layout=0, seed=A0, base=0, eng
     """Fill on the device through the public API; returns host numpy bytes."""
     par = bcn.par
     tdt = {O.FMT_U64: torch.int64, O.FMT_F64: torch.float64, O.FMT_F32: torch.float32}[fmt]
-    buf = torch.empty(n + offset, dtype=tdt, device=cuda)
+    # Sentinel-filled (all ones) rather than torch.empty: the caching allocator
+    # would otherwise hand back the previous case's (often identical) output
+    # and hide an element the kernel failed to write.
+    raw = torch.int32 if fmt == O.FMT_F32 else torch.int64
+    buf = torch.full((n + offset,), -1, dtype=raw, device=cuda).view(tdt)
     plan = par.make_plan(n, workers, par.Layout(layout))
     view = buf[offset:]
     par.fill_format(view, plan, seed, bcn.Method.BarrettModified, base, par.Format(fmt),

@@ -1,5 +1,3 @@
 # Scratch driver for one gpurun call (edited per experiment).
 set -x
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3 > gpurun_out/pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
-timeout 300 python bench.py > gpurun_out/bench_default.json 2>>gpurun_out/err.log
+timeout 1500 /usr/local/cuda/bin/compute-sanitizer --tool initcheck --print-limit 1 python tools/sanitize.py > gpurun_out/sanitize_initcheck.log 2>&1
