@@ -1,3 +1,3 @@
 # Scratch driver for one gpurun call (edited per experiment).
 set -x
-timeout 1500 /usr/local/cuda/bin/compute-sanitizer --tool initcheck --print-limit 1 python tools/sanitize.py > gpurun_out/sanitize_initcheck.log 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3 > gpurun_out/pytest_gpu.log
