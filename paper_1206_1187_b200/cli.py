@@ -67,17 +67,24 @@ def run_gen(a) -> int:
     ok = False
     try:
         done = 0
+        dtype = np.uint64 if a.format == "raw-u64" else np.float64
+        chunk_buf = np.empty(min(a.chunk, a.n), dtype=dtype)  # reused: pages touched once
         while done < a.n:
             cn = min(a.chunk, a.n - done)
             plan = par.make_plan(cn, workers, layout)
-            buf = np.empty(cn, dtype=np.uint64 if a.format == "raw-u64" else np.float64)
+            buf = chunk_buf[:cn]
             if a.format == "raw-u64":
                 par.fill_residues(buf, plan, a.seed, method, done)
             else:
                 par.fill(buf, plan, a.seed, method, done)
             if layout == par.Layout.Interleaved and not a.keep_physical:
                 buf = par.deinterleave(buf, plan)
-            sink.write(format_text(buf) if a.format == "text" else buf.astype(buf.dtype.newbyteorder("<")).tobytes())
+            if a.format == "text":
+                sink.write(format_text(buf))
+            elif sys.byteorder == "little":  # raw formats are little-endian (cli.cpp:93-135)
+                sink.write(memoryview(np.ascontiguousarray(buf)).cast("B"))
+            else:  # pragma: no cover - big-endian hosts
+                sink.write(buf.astype(buf.dtype.newbyteorder("<")).tobytes())
             done += cn
         sink.flush()
         ok = True
