@@ -53,7 +53,9 @@ __global__ void __launch_bounds__(256) k_chi_hist(const double* u, uint64_t n, i
 constexpr int kChiLaneBins = 1600;  // 32 x 4 B x 1600 = 200 KiB of shared memory
 constexpr int kChiLoads = 16;
 
-__global__ void __launch_bounds__(512) k_chi_hist_lanes(const double* u, uint64_t n, int bins,
+constexpr int kChiThreads = 1024;
+
+__global__ void __launch_bounds__(kChiThreads) k_chi_hist_lanes(const double* u, uint64_t n, int bins,
                                                         unsigned long long* counts, int* error) {
     extern __shared__ unsigned int hl[];
     const unsigned lane = threadIdx.x & 31;
@@ -284,10 +286,10 @@ cudaError_t launch_chi_hist(const double* u, uint64_t n, int bins, unsigned long
         int dev = 0, sms = 148, per_sm = 1;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chi_hist_lanes, 512, smem);
-        const uint64_t want = (n + 512 * kChiLoads - 1) / (512 * kChiLoads);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chi_hist_lanes, kChiThreads, smem);
+        const uint64_t want = (n + kChiThreads * kChiLoads - 1) / (kChiThreads * kChiLoads);
         const uint64_t cap = static_cast<uint64_t>(sms) * (per_sm > 0 ? per_sm : 1);
-        k_chi_hist_lanes<<<static_cast<unsigned>(want < cap ? want : cap), 512, smem, s>>>(u, n, bins, counts, error);
+        k_chi_hist_lanes<<<static_cast<unsigned>(want < cap ? want : cap), kChiThreads, smem, s>>>(u, n, bins, counts, error);
         return cudaGetLastError();
     }
     const size_t smem = bins <= kChiSmemBins ? static_cast<size_t>(bins) * 4 : 0;
