@@ -1,12 +1,15 @@
 #pragma once
 
 // B200 drop-in for the reference header of the same name
-// (/root/reference/proj/include/bcnrand/modred.hpp). Only the part of the
-// reduction layer the generator fill path exposes is provided: the residue
-// type, the modulus constants and the exact step oracle reduce_ref
-// (modred.hpp:16-23, :103-107). The per-step CPU reduction kernels
-// (L'Ecuyer, Barrett, modified Barrett) are replaced on the device by the
-// engines behind include/bcnrand_b200.h and are not re-exported.
+// (/root/reference/proj/include/bcnrand/modred.hpp): the residue type, the
+// constant table and its self-check, and the four host step functions of the
+// reduction layer (modred.hpp:16-159). On the GPU the step is done by the
+// engines behind include/bcnrand_b200.h; these host versions exist so code
+// (and tests) written against the reference's modred API keep working. They
+// are exact restatements of the reference's arithmetic contracts — every
+// function returns (2^53 z) mod m for z in its domain, with the reference's
+// preconditions — written independently (128-bit products instead of the
+// reference's 32-bit-halves arithmetic).
 
 #include <cstdint>
 #include <stdexcept>
@@ -24,12 +27,111 @@ namespace modred {
 inline constexpr std::uint64_t kModulus = 5559060566555523ull;  // 3^33
 inline constexpr std::uint64_t kTwo53 = std::uint64_t{1} << 53;
 
-// (2^53 z) mod m through an exact 128-bit product; z >= m is a domain error
-// (modred.hpp:103-107).
+// modred.hpp:28-48: the constants every reduction uses.
+struct ReductionConstants {
+    std::uint64_t m;      // modulus 3^33
+    std::uint64_t a_red;  // Schrage multiplier 2^25 (two stages make 2^53 with the 4 and 2 factors)
+    std::uint64_t q;      // floor(m / a_red)
+    std::uint64_t r;      // m mod a_red
+    double qinv;          // 1 / q, for the floating-point quotient of the fast Schrage stage
+    std::uint64_t mu;     // floor(2^106 / m), Barrett constant
+    int k_bits;           // 53: 2^(k-1) <= m < 2^k
+};
+
+constexpr ReductionConstants constants() {
+    return ReductionConstants{kModulus,
+                              std::uint64_t{1} << 25,
+                              kModulus >> 25,
+                              kModulus & ((std::uint64_t{1} << 25) - 1),
+                              1.0 / static_cast<double>(kModulus >> 25),
+                              static_cast<std::uint64_t>((static_cast<unsigned __int128>(1) << 106) / kModulus),
+                              53};
+}
+
+// High 64 bits of a * b (modred.hpp:57-67).
+constexpr std::uint64_t wide_mul_hi(std::uint64_t a, std::uint64_t b) {
+    return static_cast<std::uint64_t>((static_cast<unsigned __int128>(a) * b) >> 64);
+}
+
+// modred.cpp:27-41: true iff every entry is the value derived from 3^33.
+inline bool verify_constants(const ReductionConstants& c) {
+    std::uint64_t m = 1;
+    for (int i = 0; i < 33; ++i) m *= 3;
+    if (c.m != m || c.a_red != (std::uint64_t{1} << 25) || c.k_bits != 53) return false;
+    if (c.q != m / c.a_red || c.r != m % c.a_red) return false;
+    if (c.qinv != 1.0 / static_cast<double>(c.q)) return false;
+    if (c.mu != static_cast<std::uint64_t>((static_cast<unsigned __int128>(1) << 106) / m)) return false;
+    const std::uint64_t two_k = std::uint64_t{1} << c.k_bits;
+    return m < two_k && two_k < 2 * m && 4 * c.a_red * c.a_red < m;
+}
+
+namespace detail {
+
+inline void check_residue(std::uint64_t z, std::uint64_t m, const char* fn) {
+    if (z >= m) throw std::domain_error(std::string(fn) + ": residue out of range");
+}
+
+// x * a_red mod m for 0 <= x < 4m by Schrage's decomposition m = a q + r
+// (r < q): a (x mod q) - r floor(x / q) lies in (-m, a q), folded into [0, m).
+// `fast` takes the quotient from the double reciprocal and repairs it.
+inline std::uint64_t schrage_times_a(std::uint64_t x, const ReductionConstants& c, bool fast) {
+    std::uint64_t t = fast ? static_cast<std::uint64_t>(static_cast<double>(x) * c.qinv) : x / c.q;
+    if (fast) {
+        while (t * c.q > x) --t;
+        while ((t + 1) * c.q <= x) ++t;
+    }
+    const auto m = static_cast<std::int64_t>(c.m);
+    std::int64_t v = static_cast<std::int64_t>((x - t * c.q) * c.a_red) - static_cast<std::int64_t>(t * c.r);
+    while (v < 0) v += m;
+    while (v >= m) v -= m;
+    return static_cast<std::uint64_t>(v);
+}
+
+}  // namespace detail
+
+// The exact oracle (modred.hpp:103-107): 128-bit product and remainder.
 inline Residue reduce_ref(Residue z) {
-    if (z.value >= kModulus) throw std::domain_error("reduce_ref: residue out of range");
-    const auto wide = static_cast<unsigned __int128>(z.value) << 53;
-    return Residue{static_cast<std::uint64_t>(wide % kModulus)};
+    detail::check_residue(z.value, kModulus, "reduce_ref");
+    return Residue{static_cast<std::uint64_t>((static_cast<unsigned __int128>(z.value) << 53) % kModulus)};
+}
+
+// L'Ecuyer / Schrage (modred.hpp:112-124): 2^53 z = 2^25 (2 * 2^25 (4 z)).
+inline Residue lecuyer_step(Residue z, const ReductionConstants& c = constants()) {
+    detail::check_residue(z.value, c.m, "lecuyer_step");
+    const std::uint64_t a = detail::schrage_times_a(4 * z.value, c, false);
+    return Residue{detail::schrage_times_a(2 * a, c, false)};
+}
+
+inline Residue lecuyer_step_fast(Residue z, const ReductionConstants& c = constants()) {
+    detail::check_residue(z.value, c.m, "lecuyer_step_fast");
+    const std::uint64_t a = detail::schrage_times_a(4 * z.value, c, true);
+    return Residue{detail::schrage_times_a(2 * a, c, true)};
+}
+
+// Classic Barrett (modred.hpp:129-143): x = 2^53 z, q = floor(floor(x / 2^(k-1)) mu / 2^(k+1)),
+// r = x - q m mod 2^(k+1), at most two corrections.
+inline Residue barrett_step(Residue z, const ReductionConstants& c = constants()) {
+    detail::check_residue(z.value, c.m, "barrett_step");
+    const unsigned __int128 x = static_cast<unsigned __int128>(z.value) << 53;
+    const auto q1 = static_cast<std::uint64_t>(x >> (c.k_bits - 1));
+    const auto q3 = static_cast<std::uint64_t>((static_cast<unsigned __int128>(q1) * c.mu) >> (c.k_bits + 1));
+    const std::uint64_t mask = (std::uint64_t{1} << (c.k_bits + 1)) - 1;
+    std::uint64_t r = (static_cast<std::uint64_t>(x) - q3 * c.m) & mask;
+    while (r >= c.m) r -= c.m;
+    return Residue{r};
+}
+
+// The paper's modified Barrett step (modred.hpp:149-159, Fig. 3):
+// q = floor(z mu / 2^53) is floor(2^53 z / m) or one less, and the remainder
+// needs only the low 53 bits: r = 2^53 - (q m mod 2^53), one correction.
+// z = 0 is outside its domain (modred.hpp:150).
+inline Residue barrett_modified_step(Residue z, const ReductionConstants& c = constants()) {
+    if (z.value == 0) throw std::domain_error("barrett_modified_step: z = 0 not in domain");
+    detail::check_residue(z.value, c.m, "barrett_modified_step");
+    const auto q = static_cast<std::uint64_t>((static_cast<unsigned __int128>(z.value) * c.mu) >> 53);
+    std::uint64_t r = kTwo53 - ((q * c.m) & (kTwo53 - 1));
+    if (r >= c.m) r -= c.m;
+    return Residue{r};
 }
 
 }  // namespace modred
