@@ -20,21 +20,23 @@ REFTESTS = os.path.join(ROOT, "oracle", "_ref", "ref_tests_on_b200")
 DEVICE_API = os.path.join(ROOT, "tests", "cpp", "build", "test_device_api")
 
 
-REF_MODRED = os.path.join(ROOT, "oracle", "_ref", "ref_modred_tests")
+REF_HOST = os.path.join(ROOT, "oracle", "_ref", "ref_host_tests")
 
 
-def test_reference_modred_tests_pass_on_the_dropin():
+def test_reference_host_tests_pass_on_the_dropin():
     """The reference's own tests/test_modred.cpp (goldens, exhaustive and random
     agreement of all four step kernels with reduce_ref, preconditions, the
-    constant-table self-check with corrupted tables), compiled unmodified
-    against include/bcnrand/modred.hpp. Host-only: runs without a GPU."""
+    constant-table self-check with corrupted tables) and tests/test_oracle.cpp
+    (the alpha-series expansion equals seed_from_index, period law, orders),
+    compiled unmodified against include/bcnrand/{modred,oracle,generator}.hpp.
+    Host-only: runs without a GPU."""
     if os.path.isdir("/root/reference/proj"):
         r = subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp"), "ref"],
                            capture_output=True, text=True)
         assert r.returncode == 0, r.stderr
-    if not os.path.exists(REF_MODRED):
-        pytest.skip("oracle/_ref/ref_modred_tests not built and /root/reference absent")
-    r = subprocess.run([REF_MODRED], capture_output=True, text=True, timeout=600)
+    if not os.path.exists(REF_HOST):
+        pytest.skip("oracle/_ref/ref_host_tests not built and /root/reference absent")
+    r = subprocess.run([REF_HOST], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failed" in r.stdout
 
