@@ -1,7 +1,7 @@
 // Minimal doctest-compatible test shim (this repo's own code; doctest itself
 // is not vendored by the reference — SURVEY §4). Supports the subset the
 // reference's test_generator.cpp / test_parallel.cpp and tests/cpp use:
-// TEST_CASE, CHECK, CHECK_FALSE, REQUIRE, CHECK_THROWS_AS, doctest::Approx.
+// TEST_CASE, CHECK, CHECK_FALSE, CHECK_MESSAGE, REQUIRE, CHECK_THROWS_AS, doctest::Approx.
 #pragma once
 
 #include <cmath>
@@ -94,6 +94,12 @@ inline int run_all() {
 #define CHECK(...) ::doctest::detail::record(static_cast<bool>(__VA_ARGS__), #__VA_ARGS__, __FILE__, __LINE__, false)
 #define CHECK_FALSE(...) ::doctest::detail::record(!(__VA_ARGS__), "!(" #__VA_ARGS__ ")", __FILE__, __LINE__, false)
 #define REQUIRE(...) ::doctest::detail::record(static_cast<bool>(__VA_ARGS__), #__VA_ARGS__, __FILE__, __LINE__, true)
+// CHECK_MESSAGE(cond, msg): like CHECK, printing msg on failure.
+#define CHECK_MESSAGE(cond, msg)                                                                  \
+    do {                                                                                          \
+        if (!::doctest::detail::record(static_cast<bool>(cond), #cond, __FILE__, __LINE__, false)) \
+            std::fprintf(stderr, "  message: %s\n", std::string(msg).c_str());                  \
+    } while (0)
 #define CHECK_THROWS_AS(expr, exc)                                                              \
     do {                                                                                       \
         bool caught_ = false;                                                                  \
