@@ -150,6 +150,18 @@ bcn_status bcn_fill_constant(void* out, uint64_t nbytes, uint64_t pattern, int d
  * stream semantics as bcn_fill_constant. Not part of the reference API. */
 bcn_status bcn_fill_noise(void* out, uint64_t nbytes, uint64_t seed, int device, void* stream);
 
+/* One row of the reference's throughput harness (bench::run, bench.cpp:102-142)
+ * on the GPU: `repeats` fills of n doubles (plan make_plan(n, workers, layout),
+ * seed index `seed_index`) into a device buffer on `device` with `engine`
+ * (or, for engine == -1, the Constant writer over the same bytes rounded down
+ * to whole 1 KiB rows). exec_seconds = median kernel time (CUDA events),
+ * total_seconds = median wall time of the synchronous call (launch, setup and
+ * generation). With check_output, the last timed output must equal a fill
+ * with the default engine (compared by digest), else BCN_ERR_DOMAIN. */
+bcn_status bcn_bench_fill(uint64_t n, uint32_t workers, bcn_layout layout, uint64_t seed_index,
+                          int engine, int repeats, int check_output, int device,
+                          double* exec_seconds, double* total_seconds);
+
 /* Engine AUTO resolves to this engine for (format); exposed for benches. */
 int bcn_auto_engine(bcn_format format);
 

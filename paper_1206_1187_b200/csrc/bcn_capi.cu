@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <condition_variable>
 #include <cstdint>
@@ -967,6 +968,76 @@ bcn_status bcn_fill(void* out, uint64_t capacity, uint64_t n, bcn_format format,
                     bcn_engine engine, int device, void* stream) {
     return do_fill(out, capacity, n, format, workers, layout, seed_index, method, base_offset,
                    engine, device, stream);
+}
+
+bcn_status bcn_bench_fill(uint64_t n, uint32_t workers, bcn_layout layout, uint64_t seed_index,
+                          int engine, int repeats, int check_output, int device,
+                          double* exec_seconds, double* total_seconds) {
+    // bench.cpp:102-142 / :241-248, measured on the device.
+    if (!exec_seconds || !total_seconds) return fail(BCN_ERR_INVALID_ARGUMENT, "bench_fill: null output");
+    if (n == 0 || repeats < 1) return fail(BCN_ERR_INVALID_ARGUMENT, "bench_fill: n and repeats must be >= 1");
+    if (engine < -1 || engine > 6) return fail(BCN_ERR_INVALID_ARGUMENT, "bench_fill: unknown engine");
+    DeviceGuard guard;
+    DevCtx* c = nullptr;
+    bcn_status st = get_ctx(device < 0 ? 0 : device, &c);
+    if (st) return st;
+    struct Buffers {
+        void* p[2] = {nullptr, nullptr};
+        cudaEvent_t ev[2] = {nullptr, nullptr};
+        ~Buffers() {
+            for (void* q : p)
+                if (q) cudaFree(q);
+            for (cudaEvent_t e : ev)
+                if (e) cudaEventDestroy(e);
+        }
+    } b;
+    const size_t bytes = n * sizeof(double);
+    BCN_CUDA(cudaMalloc(&b.p[0], bytes + 1024));
+    BCN_CUDA(cudaEventCreate(&b.ev[0]));
+    BCN_CUDA(cudaEventCreate(&b.ev[1]));
+    const int dev = device < 0 ? 0 : device;
+    cudaStream_t s = c->stream;
+    std::vector<double> exec(static_cast<size_t>(repeats)), total(static_cast<size_t>(repeats));
+    for (int r = 0; r < repeats; ++r) {
+        BCN_CUDA(cudaStreamSynchronize(s));
+        const auto t0 = std::chrono::steady_clock::now();
+        BCN_CUDA(cudaEventRecord(b.ev[0], s));
+        if (engine == -1) {
+            const uint64_t rows_bytes = bytes / 1024 * 1024;
+            if (rows_bytes) {
+                st = bcn_fill_constant(b.p[0], rows_bytes, 0x3FE0000000000000ull, dev, s);
+                if (st) return st;
+            }
+        } else {
+            st = do_fill(b.p[0], n, n, BCN_FORMAT_F64, workers, layout, seed_index, BCN_METHOD_BARRETT_MODIFIED, 0,
+                         engine, dev, s);
+            if (st) return st;
+        }
+        BCN_CUDA(cudaEventRecord(b.ev[1], s));
+        BCN_CUDA(cudaEventSynchronize(b.ev[1]));
+        total[static_cast<size_t>(r)] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        float ms = 0.0f;
+        BCN_CUDA(cudaEventElapsedTime(&ms, b.ev[0], b.ev[1]));
+        exec[static_cast<size_t>(r)] = std::min(static_cast<double>(ms) * 1e-3, total[static_cast<size_t>(r)]);
+    }
+    auto median = [](std::vector<double>& v) {
+        std::sort(v.begin(), v.end());
+        return v.size() % 2 ? v[v.size() / 2] : 0.5 * (v[v.size() / 2 - 1] + v[v.size() / 2]);
+    };
+    *exec_seconds = median(exec);
+    *total_seconds = median(total);
+    if (check_output && engine != -1) {
+        BCN_CUDA(cudaMalloc(&b.p[1], bytes));
+        st = do_fill(b.p[1], n, n, BCN_FORMAT_F64, workers, layout, seed_index, BCN_METHOD_BARRETT_MODIFIED, 0,
+                     BCN_ENGINE_AUTO, dev, s);
+        if (st) return st;
+        uint64_t d0[3], d1[3];
+        if ((st = bcn_digest(b.p[0], n, 8, 0, d0, dev, s))) return st;
+        if ((st = bcn_digest(b.p[1], n, 8, 0, d1, dev, s))) return st;
+        if (d0[0] != d1[0] || d0[1] != d1[1] || d0[2] != d1[2])
+            return fail(BCN_ERR_DOMAIN, "bench_fill: timed output differs from an untimed fill");
+    }
+    return BCN_OK;
 }
 
 bcn_status bcn_fill_multi(void* const* outs, const int* devices, int ndev, uint64_t n,

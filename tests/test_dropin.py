@@ -3,7 +3,7 @@ ABI. Two programs written against those headers are built by tests/cpp/Makefile:
 
 * tests/cpp/build/test_dropin — this repo's C++ tests of the drop-in;
 * oracle/_ref/ref_tests_on_b200 — the REFERENCE's own unit tests
-  (tests/test_{generator,parallel,quality,selftest}.cpp, unmodified, compiled
+  (tests/test_{generator,parallel,quality,selftest,bench}.cpp, unmodified, compiled
   in place from /root/reference) linked against libbcnrand_b200.so, i.e. the
   reference's test suite for this path running on the B200 library (GPU);
 * oracle/_ref/ref_host_tests — its tests/test_{modred,oracle}.cpp against the
@@ -88,14 +88,14 @@ def test_cpp_dropin_suite(cuda):
 @pytest.mark.gpu
 def test_reference_unit_tests_pass_on_the_b200_library(cuda):
     """The reference's test_generator.cpp / test_parallel.cpp / test_quality.cpp /
-    test_selftest.cpp (34 cases, ~3.5M assertions incl. worker/layout
-    invariance, base_offset windows and the built-in selftest with a corrupted
-    constant table) pass when compiled against the drop-in headers and run on
-    the GPU."""
+    test_selftest.cpp / test_bench.cpp (40 cases, ~3.5M assertions incl.
+    worker/layout invariance, base_offset windows, the built-in selftest with a
+    corrupted constant table and the throughput harness) pass when compiled
+    against the drop-in headers and run on the GPU."""
     if not os.path.exists(REFTESTS):
         pytest.skip("oracle/_ref/ref_tests_on_b200 not built (needs /root/reference at build time)")
     out = _run(REFTESTS)
-    assert "test cases: 34 | 34 passed | 0 failed" in out, out
+    assert "test cases: 40 | 40 passed | 0 failed" in out, out
 
 
 @pytest.mark.gpu
