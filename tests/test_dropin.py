@@ -12,6 +12,7 @@ ABI. Two programs written against those headers are built by tests/cpp/Makefile:
 from __future__ import annotations
 
 import os
+import shutil
 import subprocess
 
 import pytest
@@ -23,6 +24,32 @@ DEVICE_API = os.path.join(ROOT, "tests", "cpp", "build", "test_device_api")
 
 
 REF_HOST = os.path.join(ROOT, "oracle", "_ref", "ref_host_tests")
+CMAKE_DIR = os.path.join(ROOT, "build", "cmake")
+CMAKE_DROPIN = os.path.join(CMAKE_DIR, "bcn_test_dropin")
+
+
+def test_cmake_target_bcnrand_core_builds():
+    """CMakeLists.txt exports the reference's target name `bcnrand_core`
+    (reference src/CMakeLists.txt): configure + build the library for sm_100a
+    and a program linked only against `bcnrand_core`, as a reference user's
+    CMake project would."""
+    cmake = shutil.which("cmake")
+    if cmake is None:
+        pytest.skip("cmake not installed")
+    os.makedirs(CMAKE_DIR, exist_ok=True)
+    env = dict(os.environ, CUDACXX=os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc"))
+    gen = ["-G", "Ninja"] if shutil.which("ninja") else []
+    r = subprocess.run([cmake, "-S", ROOT, "-B", CMAKE_DIR, *gen, "-DBCN_BUILD_TESTS=ON"],
+                       capture_output=True, text=True, env=env, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    r = subprocess.run([cmake, "--build", CMAKE_DIR, "-j", "8"], capture_output=True, text=True,
+                       env=env, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert os.path.exists(CMAKE_DROPIN)
+    elf = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf",
+                          os.path.join(CMAKE_DIR, "libbcnrand_b200.so")], capture_output=True, text=True)
+    if elf.returncode == 0:
+        assert "sm_100a" in elf.stdout and "sm_52" not in elf.stdout, elf.stdout
 
 
 def test_reference_host_tests_pass_on_the_dropin():
@@ -96,6 +123,15 @@ def test_reference_unit_tests_pass_on_the_b200_library(cuda):
         pytest.skip("oracle/_ref/ref_tests_on_b200 not built (needs /root/reference at build time)")
     out = _run(REFTESTS)
     assert "test cases: 40 | 40 passed | 0 failed" in out, out
+
+
+@pytest.mark.gpu
+def test_cmake_built_dropin_suite(cuda):
+    """The drop-in test program built through CMakeLists.txt's `bcnrand_core`
+    target (and its own libbcnrand_b200.so) passes on the GPU."""
+    if not os.path.exists(CMAKE_DROPIN):
+        pytest.skip("build/cmake/bcn_test_dropin not built")
+    _run(CMAKE_DROPIN)
 
 
 @pytest.mark.gpu
