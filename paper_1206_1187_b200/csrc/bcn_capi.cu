@@ -691,6 +691,15 @@ CopyPool& copy_pool() {
 bcn_status fill_host(FillJob& j, char* out, bool out_pinned) {
     DevCtx* c = j.ctx;
     std::lock_guard<std::mutex> lock(c->mu);
+    // On an early (error) return no DMA into the caller's buffer or the
+    // staging buffers may still be in flight: drain both copy streams.
+    struct Drain {
+        DevCtx* c;
+        ~Drain() {
+            cudaStreamSynchronize(c->copy[0]);
+            cudaStreamSynchronize(c->copy[1]);
+        }
+    } drain{c};
     const int isz = format_itemsize(j.fmt);
     const uint64_t chunk_items = (64ull << 20) / isz;  // 64 MiB per chunk
     bcn_status st = ensure_scratch(c, chunk_items * isz, !out_pinned);
@@ -1049,6 +1058,19 @@ bcn_status bcn_fill_multi(void* const* outs, const int* devices, int ndev, uint6
     if (st) return st;
     if ((st = validate_enums(format, 0, 3, engine))) return st;
     if ((st = check_seed(seed_index))) return st;
+    if (plan.wpw >= (1ull << 40))
+        return fail(BCN_ERR_INVALID_ARGUMENT, "fill_multi: n must be below 2^40 per device");
+    const int isz = format_itemsize(format);
+    for (uint32_t g = 0; g < plan.workers; ++g) {
+        if (!outs[g]) return fail(BCN_ERR_INVALID_ARGUMENT, "fill_multi: null shard buffer");
+        if (reinterpret_cast<uintptr_t>(outs[g]) % isz)
+            return fail(BCN_ERR_INVALID_ARGUMENT, "fill_multi: shard buffer not aligned to its item size");
+        int dev = devices[g];
+        PtrKind kind;
+        if ((st = classify(outs[g], &dev, &kind))) return st;
+        if (kind != PtrKind::Device)
+            return fail(BCN_ERR_INVALID_ARGUMENT, "fill_multi: shard buffers must be device memory");
+    }
     std::vector<bcn_status> res(plan.workers, BCN_OK);
     std::vector<std::string> msg(plan.workers);
     std::vector<std::thread> pool;
@@ -1102,13 +1124,26 @@ bcn_status bcn_deinterleave(const void* in, void* out, uint64_t n, uint32_t work
     if ((st = caller_stream(c, stream, &s))) return st;
     const void* din = in;
     void* dout = out;
-    void* tmp = nullptr;
     const size_t bytes = n * itemsize;
+    // Host buffers: staged through one device temporary, freed (after the
+    // stream drains) on every exit path.
+    struct Temp {
+        void* p = nullptr;
+        cudaStream_t s = nullptr;
+        ~Temp() {
+            if (p) {
+                cudaStreamSynchronize(s);
+                cudaFree(p);
+            }
+        }
+    } tmp;
+    tmp.s = s;
     if (kin != PtrKind::Device) {
-        BCN_CUDA(cudaMalloc(&tmp, 2 * bytes));
-        BCN_CUDA(cudaMemcpyAsync(tmp, in, bytes, cudaMemcpyHostToDevice, s));
-        din = tmp;
-        dout = static_cast<char*>(tmp) + bytes;
+        if (n >= (1ull << 40)) return fail(BCN_ERR_INVALID_ARGUMENT, "deinterleave: n must be below 2^40 per call");
+        BCN_CUDA(cudaMalloc(&tmp.p, 2 * bytes));
+        BCN_CUDA(cudaMemcpyAsync(tmp.p, in, bytes, cudaMemcpyHostToDevice, s));
+        din = tmp.p;
+        dout = static_cast<char*>(tmp.p) + bytes;
     }
     const uint64_t sc = p.short_count();
     TransposeArgs t;
@@ -1130,10 +1165,9 @@ bcn_status bcn_deinterleave(const void* in, void* out, uint64_t n, uint32_t work
         cudaError_t e = launch_transpose(t, s);
         if (e != cudaSuccess) return cuda_fail(e, "deinterleave launch");
     }
-    if (tmp) {
+    if (tmp.p) {
         BCN_CUDA(cudaMemcpyAsync(out, dout, bytes, cudaMemcpyDeviceToHost, s));
         BCN_CUDA(cudaStreamSynchronize(s));
-        cudaFree(tmp);
     } else if (!stream) {
         BCN_CUDA(cudaStreamSynchronize(s));
     }
@@ -1150,6 +1184,11 @@ bcn_status bcn_seed_states(const uint64_t* a, const uint64_t* k, uint64_t* out, 
     bcn_status st = classify(out, &dev, &kind);
     if (st) return st;
     if (kind != PtrKind::Device) return fail(BCN_ERR_INVALID_ARGUMENT, "seed_states: buffers must be device memory");
+    for (const void* in : {static_cast<const void*>(a), static_cast<const void*>(k)}) {
+        if ((st = classify(in, &dev, &kind))) return st;
+        if (kind != PtrKind::Device)
+            return fail(BCN_ERR_INVALID_ARGUMENT, "seed_states: buffers must be device memory");
+    }
     DevCtx* c = nullptr;
     if ((st = get_ctx(dev, &c))) return st;
     std::lock_guard<std::mutex> scratch_lock(c->small_mu);

@@ -454,6 +454,50 @@ def test_fill_multi_concatenation(bcn, cuda, oracle):
     assert np.array_equal(bits(got), bits(oracle.fill(n, O.FMT_F64, base_offset=31, workers=2)))
 
 
+def test_cabi_rejects_host_buffers_where_device_memory_is_required(bcn, cuda, oracle):
+    """C callers (no Python guard): host pointers passed to device-only entry
+    points are rejected with BCN_ERR_INVALID_ARGUMENT before any launch, and
+    the context stays usable (no sticky illegal-address error)."""
+    import ctypes
+    h = bcn._lib.lib()
+    host_a = np.full(4, A0, dtype=np.uint64)
+    host_k = np.zeros(4, dtype=np.uint64)
+    dev_a = torch.from_numpy(host_a.view(np.int64)).to(cuda)
+    dev_k = torch.from_numpy(host_k.view(np.int64)).to(cuda)
+    out = torch.empty(4, dtype=torch.int64, device=cuda)
+    vp = ctypes.c_void_p
+    for a_ptr, k_ptr in ((host_a.ctypes.data, dev_k.data_ptr()), (dev_a.data_ptr(), host_k.ctypes.data)):
+        st = h.bcn_seed_states(vp(a_ptr), vp(k_ptr), vp(out.data_ptr()), 4, 0, 0, None)
+        assert st == 1 and b"device memory" in h.bcn_last_error()
+    host_out = np.empty(100, dtype=np.float64)
+    ptrs = (vp * 1)(host_out.ctypes.data)
+    devs = (ctypes.c_int * 1)(0)
+    st = h.bcn_fill_multi(ptrs, devs, 1, 100, 1, A0, 0, 0)
+    assert st == 1 and b"device memory" in h.bcn_last_error()
+    ptrs = (vp * 1)(None)
+    assert h.bcn_fill_multi(ptrs, devs, 1, 100, 1, A0, 0, 0) == 1
+    # still healthy: a real call on the same context is bit-exact
+    got = bcn.device.seed_states(dev_a, dev_k).cpu().numpy().view(np.uint64)
+    assert got.tolist() == [oracle.state_at(A0, 0)] * 4
+
+
+def test_host_deinterleave_releases_its_staging(bcn, cuda, oracle):
+    """The host-buffer deinterleave stages through a device temporary that is
+    released on every exit path: repeated host calls keep the reference order
+    and leave device memory where it was."""
+    n, w = 1_000_003, 7
+    phys = oracle.fill(n, O.FMT_U64, workers=w, layout=O.INTERLEAVED)
+    want = oracle.fill(n, O.FMT_U64)
+    plan = bcn.par.make_plan(n, w, bcn.Layout.Interleaved)
+    bcn.par.deinterleave(phys, plan)
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info(cuda)[0]
+    for _ in range(4):
+        got = bcn.par.deinterleave(phys, plan)
+        assert np.array_equal(np.asarray(got).view(np.uint64), want.view(np.uint64))
+    assert abs(torch.cuda.mem_get_info(cuda)[0] - free0) < (4 << 20)
+
+
 def test_scalar_generator_api(bcn, cuda, oracle):
     g = bcn.gen
     s = g.seed_from_index(A0)
