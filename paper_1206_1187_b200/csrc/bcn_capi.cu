@@ -1289,6 +1289,10 @@ bcn_status bcn_fill_noise(void* out, uint64_t nbytes, uint64_t seed, int device,
 }  // extern "C"
 
 // ------------------------------------------------------------ quality suite
+namespace {
+constexpr uint64_t kMaxQualityItems = 1ull << 40;  // keeps n * 8 far from overflow
+}
+
 extern "C" {
 
 bcn_status bcn_chi_square_uniformity(const double* samples, uint64_t n, int bins, double* statistic,
@@ -1301,6 +1305,7 @@ bcn_status bcn_chi_square_uniformity(const double* samples, uint64_t n, int bins
     const double expected = static_cast<double>(n) / bins;
     if (expected < 20.0) return fail(BCN_ERR_INVALID_ARGUMENT, "chi_square: expected count per bin below 20");
     if (!samples) return fail(BCN_ERR_INVALID_ARGUMENT, "chi_square: null samples");
+    if (n >= kMaxQualityItems) return fail(BCN_ERR_INVALID_ARGUMENT, "chi_square: n must be below 2^40");
     DeviceInput in;
     DevCtx* c = nullptr;
     cudaStream_t s;
@@ -1340,6 +1345,7 @@ bcn_status bcn_monobit_mantissa(const uint64_t* residues, uint64_t n, double* st
     if (!statistic || !worst_bit || !pass) return fail(BCN_ERR_INVALID_ARGUMENT, "monobit: null output");
     if (n < 100000) return fail(BCN_ERR_INVALID_ARGUMENT, "monobit: need at least 1e5 residues");
     if (!residues) return fail(BCN_ERR_INVALID_ARGUMENT, "monobit: null residues");
+    if (n >= kMaxQualityItems) return fail(BCN_ERR_INVALID_ARGUMENT, "monobit: n must be below 2^40");
     DeviceInput in;
     DevCtx* c = nullptr;
     cudaStream_t s;
@@ -1385,6 +1391,10 @@ bcn_status bcn_serial_correlation(const double* samples, uint64_t n, int lag, do
     if (lag < 1) return fail(BCN_ERR_INVALID_ARGUMENT, "serial_correlation: lag must be positive");
     if (n < 100000) return fail(BCN_ERR_INVALID_ARGUMENT, "serial_correlation: need at least 1e5 samples");
     if (!samples) return fail(BCN_ERR_INVALID_ARGUMENT, "serial_correlation: null samples");
+    if (n >= kMaxQualityItems) return fail(BCN_ERR_INVALID_ARGUMENT, "serial_correlation: n must be below 2^40");
+    // The reference reads past the span when lag >= n (quality.cpp:94); rejected here.
+    if (static_cast<uint64_t>(lag) >= n)
+        return fail(BCN_ERR_INVALID_ARGUMENT, "serial_correlation: lag must be below the sample count");
     DeviceInput in;
     DevCtx* c = nullptr;
     cudaStream_t s;

@@ -566,6 +566,9 @@ def test_quality_suite_matches_reference(bcn, cuda, oracle, reference):
         q.chi_square_uniformity(np.full(1000, 0.5), 100)
     with pytest.raises(bcn.InvalidArgument):
         q.chi_square_uniformity(np.array([0.5] * 100 + [1.5] * 100000), 10)
+    # lag >= n is out-of-bounds in the reference (quality.cpp:94); rejected here
+    with pytest.raises(bcn.InvalidArgument):
+        q.serial_correlation(u[:100000], 100000)
 
 
 # ---------------------------------------------------------- multi-rank bench
