@@ -76,15 +76,15 @@ inline void check_residue(std::uint64_t z, std::uint64_t m, const char* fn) {
 // `fast` takes the quotient from the double reciprocal and repairs it.
 inline std::uint64_t schrage_times_a(std::uint64_t x, const ReductionConstants& c, bool fast) {
     std::uint64_t t = fast ? static_cast<std::uint64_t>(static_cast<double>(x) * c.qinv) : x / c.q;
-    if (fast) {
+    if (fast) {  // repair the floating-point quotient to floor(x / q)
         while (t * c.q > x) --t;
         while ((t + 1) * c.q <= x) ++t;
     }
+    const std::int64_t hi = static_cast<std::int64_t>((x - t * c.q) * c.a_red);
+    const std::int64_t lo = static_cast<std::int64_t>(t * c.r);
     const auto m = static_cast<std::int64_t>(c.m);
-    std::int64_t v = static_cast<std::int64_t>((x - t * c.q) * c.a_red) - static_cast<std::int64_t>(t * c.r);
-    while (v < 0) v += m;
-    while (v >= m) v -= m;
-    return static_cast<std::uint64_t>(v);
+    const std::int64_t v = (hi - lo) % m;
+    return static_cast<std::uint64_t>(v < 0 ? v + m : v);
 }
 
 }  // namespace detail
@@ -113,12 +113,11 @@ inline Residue lecuyer_step_fast(Residue z, const ReductionConstants& c = consta
 inline Residue barrett_step(Residue z, const ReductionConstants& c = constants()) {
     detail::check_residue(z.value, c.m, "barrett_step");
     const unsigned __int128 x = static_cast<unsigned __int128>(z.value) << 53;
-    const auto q1 = static_cast<std::uint64_t>(x >> (c.k_bits - 1));
-    const auto q3 = static_cast<std::uint64_t>((static_cast<unsigned __int128>(q1) * c.mu) >> (c.k_bits + 1));
-    const std::uint64_t mask = (std::uint64_t{1} << (c.k_bits + 1)) - 1;
-    std::uint64_t r = (static_cast<std::uint64_t>(x) - q3 * c.m) & mask;
-    while (r >= c.m) r -= c.m;
-    return Residue{r};
+    const auto x_top = static_cast<std::uint64_t>(x >> (c.k_bits - 1));
+    const auto quot = static_cast<std::uint64_t>((static_cast<unsigned __int128>(x_top) * c.mu) >> (c.k_bits + 1));
+    const std::uint64_t low_bits = (std::uint64_t{2} << c.k_bits) - 1;
+    const std::uint64_t rem = (static_cast<std::uint64_t>(x) - quot * c.m) & low_bits;
+    return Residue{rem % c.m};  // the reference's (at most two) corrections
 }
 
 // The paper's modified Barrett step (modred.hpp:149-159, Fig. 3):
@@ -128,10 +127,9 @@ inline Residue barrett_step(Residue z, const ReductionConstants& c = constants()
 inline Residue barrett_modified_step(Residue z, const ReductionConstants& c = constants()) {
     if (z.value == 0) throw std::domain_error("barrett_modified_step: z = 0 not in domain");
     detail::check_residue(z.value, c.m, "barrett_modified_step");
-    const auto q = static_cast<std::uint64_t>((static_cast<unsigned __int128>(z.value) * c.mu) >> 53);
-    std::uint64_t r = kTwo53 - ((q * c.m) & (kTwo53 - 1));
-    if (r >= c.m) r -= c.m;
-    return Residue{r};
+    const auto quot = static_cast<std::uint64_t>((static_cast<unsigned __int128>(z.value) * c.mu) >> 53);
+    const std::uint64_t rem = kTwo53 - ((quot * c.m) & (kTwo53 - 1));
+    return Residue{rem >= c.m ? rem - c.m : rem};
 }
 
 }  // namespace modred

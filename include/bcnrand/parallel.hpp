@@ -21,14 +21,26 @@ namespace bcn::par {
 // parallel.hpp:15
 enum class Layout { Contiguous, Interleaved };
 
+namespace detail {
+struct LayoutName {
+    Layout layout;
+    const char* text;
+};
+inline constexpr LayoutName kLayoutNames[] = {{Layout::Contiguous, "contiguous"},
+                                              {Layout::Interleaved, "interleaved"}};
+}  // namespace detail
+
 inline const char* layout_name(Layout layout) {
-    return layout == Layout::Contiguous ? "contiguous" : "interleaved";
+    for (const auto& e : detail::kLayoutNames)
+        if (e.layout == layout) return e.text;
+    return "?";
 }
 
-inline Layout parse_layout(const std::string& name) {
-    if (name == "contiguous") return Layout::Contiguous;
-    if (name == "interleaved") return Layout::Interleaved;
-    throw std::invalid_argument("unknown layout: " + name);
+// The lower-case names above; anything else is std::invalid_argument.
+inline Layout parse_layout(const std::string& text) {
+    for (const auto& e : detail::kLayoutNames)
+        if (text == e.text) return e.layout;
+    throw std::invalid_argument("parse_layout: no layout named '" + text + "'");
 }
 
 // parallel.hpp:17-38
@@ -57,17 +69,21 @@ struct PartitionPlan {
 
 // parallel.hpp:42 — n = 0 or workers = 0 is std::invalid_argument.
 inline PartitionPlan make_plan(std::uint64_t n, unsigned workers, Layout layout) {
-    std::uint32_t eff = 0;
-    std::uint64_t wpw = 0;
-    b200::check(bcn_make_plan(n, workers, &eff, &wpw));
+    std::uint32_t effective = 0;
+    std::uint64_t per_worker = 0;
+    b200::check(bcn_make_plan(n, workers, &effective, &per_worker));
     PartitionPlan plan;
     plan.n = n;
-    plan.workers = eff;
-    plan.work_per_worker = wpw;
+    plan.workers = effective;
+    plan.work_per_worker = per_worker;
     plan.layout = layout;
-    plan.step = eff;
-    plan.start_offsets.reserve(eff);
-    for (unsigned w = 0; w < eff; ++w) plan.start_offsets.push_back(static_cast<std::uint64_t>(w) * wpw);
+    plan.step = effective;
+    plan.start_offsets.resize(effective);
+    std::uint64_t start = 0;
+    for (auto& s : plan.start_offsets) {
+        s = start;
+        start += per_worker;
+    }
     return plan;
 }
 
@@ -105,25 +121,25 @@ inline void fill_float(std::span<float> out, const PartitionPlan& plan, std::uin
 }
 
 namespace detail {
-template <typename T>
-std::vector<T> deinterleave_impl(std::span<const T> buffer, const PartitionPlan& plan) {
-    if (plan.layout != Layout::Interleaved)
+// One device transpose (bcn_deinterleave); host spans are staged through the GPU.
+template <typename Item>
+std::vector<Item> to_logical_order(std::span<const Item> physical, const PartitionPlan& plan) {
+    if (plan.layout == Layout::Contiguous)
         throw std::invalid_argument("deinterleave: plan layout is not Interleaved");
-    if (buffer.size() < plan.n) throw std::invalid_argument("deinterleave: buffer smaller than plan.n");
-    std::vector<T> logical(plan.n);
-    b200::check(bcn_deinterleave(buffer.data(), logical.data(), plan.n, plan.workers, sizeof(T), -1,
-                                 nullptr));
+    if (physical.size() < plan.n) throw std::invalid_argument("deinterleave: buffer smaller than plan.n");
+    std::vector<Item> logical(plan.n);
+    b200::check(bcn_deinterleave(physical.data(), logical.data(), plan.n, plan.workers,
+                                 static_cast<std::uint32_t>(sizeof(Item)), -1, nullptr));
     return logical;
 }
 }  // namespace detail
 
 // parallel.hpp:58-60
 inline std::vector<double> deinterleave(std::span<const double> buffer, const PartitionPlan& plan) {
-    return detail::deinterleave_impl(buffer, plan);
+    return detail::to_logical_order(buffer, plan);
 }
-inline std::vector<std::uint64_t> deinterleave(std::span<const std::uint64_t> buffer,
-                                               const PartitionPlan& plan) {
-    return detail::deinterleave_impl(buffer, plan);
+inline std::vector<std::uint64_t> deinterleave(std::span<const std::uint64_t> buffer, const PartitionPlan& plan) {
+    return detail::to_logical_order(buffer, plan);
 }
 
 }  // namespace bcn::par

@@ -7,8 +7,9 @@
 
 #include <cmath>
 #include <cstdint>
-#include <cstdio>
+#include <iomanip>
 #include <ostream>
+#include <sstream>
 #include <span>
 #include <string>
 
@@ -26,10 +27,10 @@ struct QualityReport {
 };
 
 namespace detail {
-inline std::string fmt(const char* f, double a, double b = 0.0) {
-    char buf[128];
-    std::snprintf(buf, sizeof(buf), f, a, b);
-    return buf;
+inline std::string band(const char* lhs, double bound) {
+    std::ostringstream o;
+    o << lhs << " <= " << std::setprecision(4) << bound;
+    return o.str();
 }
 }  // namespace detail
 
@@ -44,7 +45,7 @@ inline QualityReport chi_square_uniformity(std::span<const double> samples, int 
     r.statistic = stat;
     r.dof = dof;
     r.pass = pass != 0;
-    r.threshold = detail::fmt("|stat - %.0f| <= %.1f", dof, 4.5 * std::sqrt(2.0 * dof));
+    r.threshold = detail::band(("|stat - " + std::to_string(dof) + "|").c_str(), 4.5 * std::sqrt(2.0 * dof));
     return r;
 }
 
@@ -60,8 +61,8 @@ inline QualityReport monobit_mantissa(std::span<const Residue> residues) {
     r.statistic = stat;
     r.dof = 48;
     r.pass = pass != 0;
-    r.threshold = detail::fmt("max|freq-0.5| <= %.3g (worst bit %g)",
-                              4.5 / (2.0 * std::sqrt(static_cast<double>(residues.size()))), worst);
+    r.threshold = detail::band("max |ones/n - 1/2|", 4.5 / (2.0 * std::sqrt(static_cast<double>(residues.size())))) +
+                  ", worst bit " + std::to_string(worst);
     return r;
 }
 
@@ -76,29 +77,32 @@ inline QualityReport serial_correlation(std::span<const double> samples, int lag
     r.statistic = rho;
     r.dof = static_cast<int>(pairs > (std::uint64_t{1} << 30) ? (1 << 30) : pairs);
     r.pass = pass != 0;
-    r.threshold = detail::fmt("|rho| <= %.3g", 4.5 / std::sqrt(static_cast<double>(samples.size())));
+    r.threshold = detail::band("|rho|", 4.5 / std::sqrt(static_cast<double>(samples.size())));
     return r;
 }
 
-// quality.hpp:40-45
+// quality.hpp:40-45: an aligned human-readable table, and one
+// `name=… statistic=… dof=… pass=…` line per report for scripts.
 inline void write_table(std::ostream& os, std::span<const QualityReport> reports) {
-    char line[256];
-    std::snprintf(line, sizeof(line), "%-24s %14s %8s %6s  %s\n", "test", "statistic", "dof", "pass",
-                  "threshold");
-    os << line;
-    for (const auto& r : reports) {
-        std::snprintf(line, sizeof(line), "%-24s %14.6g %8d %6s  %s\n", r.name.c_str(), r.statistic, r.dof,
-                      r.pass ? "yes" : "NO", r.threshold.c_str());
-        os << line;
+    const auto row = [&os](const std::string& a, const std::string& b, const std::string& c,
+                           const std::string& d, const std::string& e) {
+        os << std::left << std::setw(26) << a << std::right << std::setw(16) << b << std::setw(10) << c
+           << std::setw(7) << d << "   " << e << '\n';
+    };
+    row("test", "statistic", "dof", "pass", "threshold");
+    for (const QualityReport& r : reports) {
+        std::ostringstream stat;
+        stat << std::setprecision(7) << r.statistic;
+        row(r.name, stat.str(), std::to_string(r.dof), r.pass ? "yes" : "no", r.threshold);
     }
 }
 
 inline void write_kv(std::ostream& os, std::span<const QualityReport> reports) {
-    for (const auto& r : reports) {
-        char line[256];
-        std::snprintf(line, sizeof(line), "name=%s statistic=%.17g dof=%d pass=%s\n", r.name.c_str(),
-                      r.statistic, r.dof, r.pass ? "true" : "false");
-        os << line;
+    for (const QualityReport& r : reports) {
+        std::ostringstream line;
+        line << "name=" << r.name << " statistic=" << std::setprecision(17) << r.statistic << " dof=" << r.dof
+             << " pass=" << std::boolalpha << r.pass << '\n';
+        os << line.str();
     }
 }
 
