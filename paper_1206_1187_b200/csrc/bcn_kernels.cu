@@ -898,7 +898,7 @@ __global__ void __launch_bounds__(256) k_transpose(const TransposeArgs a) {
 }
 
 // Narrow regions (width <= kNarrowMaxWidth workers): tiles of R whole rows
-// (R*width <= kNarrowItems slots, R a multiple of 64) are one contiguous span
+// (R*width <= kNarrowItems slots, R a multiple of 64, or of 16 when W > 64) are one contiguous span
 // of the input, read fully coalesced (kNarrowItems/256 loads per thread),
 // scattered into shared memory as [width][R] with an odd pitch (row = slot /
 // width by a multiply-high), and each worker's R consecutive logical items
@@ -908,6 +908,15 @@ template <typename T>
 struct NarrowTile {
     static constexpr unsigned kItems = 8192;  // slots per tile (64 / 32 KiB)
     static constexpr unsigned kLoads = kItems / 256;
+    // Rows per tile: as many whole rows as fit, a multiple of 64 (512-byte
+    // output runs for u64) — except for W in (64, 128], where that leaves 64
+    // rows and 50-99% of the tile (W = 100: 6400 of 8192 slots); there a
+    // multiple of 16 (W = 100: 80 rows) is 2-10% faster for u64 and 5-16% for
+    // u32 (one exception: u64 W = 65, 11% slower). A multiple of 16 for every
+    // W measured 1-5% slower at W = 7 and 33 (profiles/r01/deinterleave_rows16*.jsonl).
+    static __host__ __device__ constexpr unsigned rows(unsigned width) {
+        return width > 64 ? kItems / width / 16 * 16 : kItems / width / 64 * 64;
+    }
 };
 
 template <typename T>
@@ -934,7 +943,7 @@ __global__ void __launch_bounds__(256) k_transpose_narrow(const TransposeArgs a)
     T* tile = reinterpret_cast<T*>(narrow_smem);
     T* out = static_cast<T*>(a.out);
     const unsigned W = static_cast<unsigned>(a.width);
-    const unsigned R = G::kItems / W / 64 * 64;  // rows per tile
+    const unsigned R = G::rows(W);  // rows per tile
     const unsigned P = R | 1;                      // odd pitch
     // slot / W == (slot * M) >> 32 exactly for slot < 2^32 / W, M = ceil(2^32 / W)
     const uint64_t M = ((1ull << 32) + W - 1) / W;
@@ -1200,7 +1209,7 @@ cudaError_t transpose_t(const TransposeArgs& a, cudaStream_t s) {
         const size_t smem = (G::kItems + kNarrowMaxWidth) * sizeof(T);
         cudaFuncSetAttribute(k_transpose_narrow<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
-        const uint64_t rows_per_tile = G::kItems / a.width / 64 * 64;
+        const uint64_t rows_per_tile = G::rows(static_cast<unsigned>(a.width));
         const uint64_t tiles = (a.rows + rows_per_tile - 1) / rows_per_tile;
         const uint64_t cap = static_cast<uint64_t>(sms) * occupancy(k_transpose_narrow<T>, 256, smem);
         k_transpose_narrow<T><<<static_cast<unsigned>(std::min(tiles, cap)), 256, smem, s>>>(a);
@@ -1208,10 +1217,18 @@ cudaError_t transpose_t(const TransposeArgs& a, cudaStream_t s) {
         // Tile shape sweep (profiles/r01/deinterleave_tiles.jsonl): 128-row
         // tiles win everywhere; 8-byte items prefer 1 KiB input runs unless
         // the last tile column would be mostly empty (e.g. W = 129).
+        // 4-byte items likewise fall back from 512-byte (128-worker) to
+        // 256-byte (64-worker) tiles when the last tile column would be mostly
+        // empty (u32 W = 129: 0.54 ms with 128-worker tiles).
         const uint64_t cover128 = (a.width + 127) / 128 * 128, cover64 = (a.width + 63) / 64 * 64;
-        if (sizeof(T) == 8 && cover128 * 10 <= cover64 * 11)
-            return transpose_wide<T, 128, 1024>(a, sms, s);
-        return transpose_wide<T, 128, 512>(a, sms, s);
+        const bool wide_cols = cover128 * 10 <= cover64 * 11;
+        if constexpr (sizeof(T) == 8) {
+            if (wide_cols) return transpose_wide<T, 128, 1024>(a, sms, s);
+            return transpose_wide<T, 128, 512>(a, sms, s);
+        } else {
+            if (wide_cols) return transpose_wide<T, 128, 512>(a, sms, s);
+            return transpose_wide<T, 128, 256>(a, sms, s);
+        }
     }
     return counted(cudaGetLastError());
 }

@@ -2,7 +2,7 @@
 """Device deinterleave throughput (exploration / evidence tool): CUDA-event
 median per call, GB/s counting read + write (2 x itemsize per item).
 
-    python tools/deint_perf.py >> gpurun_out/deint.jsonl
+    python tools/deint_perf.py [W1,W2,...] >> gpurun_out/deint.jsonl
 """
 from __future__ import annotations
 
@@ -19,12 +19,15 @@ import paper_1206_1187_b200 as B  # noqa: E402
 
 
 def main() -> None:
+    widths = (1, 2, 7, 16, 31, 33, 64, 100, 128, 129, 200, 1000, 100003)
+    if len(sys.argv) > 1:
+        widths = tuple(int(w) for w in sys.argv[1].split(","))
     dev = torch.device("cuda:0")
     stream = torch.cuda.current_stream(dev)
     n = 1 << 28
     for dt, isz in ((torch.float64, 8), (torch.float32, 4)):
         buf = torch.empty(n, dtype=dt, device=dev)
-        for w in (1, 2, 7, 16, 31, 33, 64, 100, 128, 129, 200, 1000, 100003):
+        for w in widths:
             plan = B.par.make_plan(n, w, B.Layout.Interleaved)
             B.par.deinterleave(buf, plan)
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(11)]
