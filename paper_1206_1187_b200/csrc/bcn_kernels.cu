@@ -841,11 +841,25 @@ struct WideTile {
     static_assert(kCols <= 256 && 256 % kCols == 0 && kRows % (256 / kCols) == 0, "tile shape");
 };
 
+// Tile t -> (first worker, first row).
+template <class G>
+__device__ __forceinline__ void wide_origin(const TransposeArgs& a, uint64_t t, uint64_t ntw, uint64_t nrb,
+                                            uint64_t& w0, uint64_t& i0) {
+    if (a.order) {
+        w0 = (t / nrb) * G::kCols;
+        i0 = (t % nrb) * G::kRows;
+    } else {
+        w0 = (t % ntw) * G::kCols;
+        i0 = (t / ntw) * G::kRows;
+    }
+}
+
 template <typename T, class G>
-__device__ __forceinline__ void wide_load(const TransposeArgs& a, uint64_t t, uint64_t ntw,
+__device__ __forceinline__ void wide_load(const TransposeArgs& a, uint64_t t, uint64_t ntw, uint64_t nrb,
                                           T (&v)[G::kLoads]) {
     const T* in = static_cast<const T*>(a.in);
-    const uint64_t w0 = (t % ntw) * G::kCols, i0 = (t / ntw) * G::kRows;
+    uint64_t w0, i0;
+    wide_origin<G>(a, t, ntw, nrb, w0, i0);
     const T* src = in + a.p0 + i0 * a.width + w0;
     constexpr int kRowStep = 256 / G::kCols;  // rows a thread advances per load
     const int r = threadIdx.x / G::kCols, c = threadIdx.x % G::kCols;
@@ -870,18 +884,20 @@ __global__ void __launch_bounds__(256) k_transpose(const TransposeArgs a) {
     T* tile = reinterpret_cast<T*>(wide_smem);
     T* out = static_cast<T*>(a.out);
     const uint64_t ntw = (a.width + G::kCols - 1) / G::kCols;
-    const uint64_t ntiles = ntw * ((a.rows + G::kRows - 1) / G::kRows);
+    const uint64_t nrb = (a.rows + G::kRows - 1) / G::kRows;
+    const uint64_t ntiles = ntw * nrb;
     constexpr int kRowStep = 256 / G::kCols;
     const int r = threadIdx.x / G::kCols, c = threadIdx.x % G::kCols;
     T v[G::kLoads];
     uint64_t t = blockIdx.x;
-    if (t < ntiles) wide_load<T, G>(a, t, ntw, v);
+    if (t < ntiles) wide_load<T, G>(a, t, ntw, nrb, v);
     for (; t < ntiles; t += gridDim.x) {
 #pragma unroll
         for (int j = 0; j < G::kLoads; ++j) tile[(r + kRowStep * j) * G::kPitch + c] = v[j];
         __syncthreads();
-        if (t + gridDim.x < ntiles) wide_load<T, G>(a, t + gridDim.x, ntw, v);  // prefetch
-        const uint64_t w0 = (t % ntw) * G::kCols, i0 = (t / ntw) * G::kRows;
+        if (t + gridDim.x < ntiles) wide_load<T, G>(a, t + gridDim.x, ntw, nrb, v);  // prefetch
+        uint64_t w0, i0;
+        wide_origin<G>(a, t, ntw, nrb, w0, i0);
         T* dst = out + w0 * a.wpw + a.i_base + i0;
         const int i = threadIdx.x % G::kRows;  // item within the worker's run
         const int wq = threadIdx.x / G::kRows;  // first worker of this thread
@@ -1193,9 +1209,18 @@ cudaError_t transpose_wide(const TransposeArgs& a, int sms, cudaStream_t s) {
     const size_t smem = static_cast<size_t>(G::kRows) * G::kPitch * sizeof(T);
     cudaFuncSetAttribute(k_transpose<T, ROWS, BYTES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
-    const uint64_t tiles = ((a.width + G::kCols - 1) / G::kCols) * ((a.rows + G::kRows - 1) / G::kRows);
+    const uint64_t nrb = (a.rows + G::kRows - 1) / G::kRows;
+    const uint64_t tiles = ((a.width + G::kCols - 1) / G::kCols) * nrb;
     const uint64_t cap = static_cast<uint64_t>(sms) * occupancy(k_transpose<T, ROWS, BYTES>, 256, smem);
-    k_transpose<T, ROWS, BYTES><<<static_cast<unsigned>(std::min(tiles, cap)), 256, smem, s>>>(a);
+    const uint64_t grid = std::min(tiles, cap);
+    // Tile order: with few row blocks per worker (very wide regions: short
+    // per-worker runs), walking row blocks fastest keeps every worker's whole
+    // output run in flight at once: +8-33% at W >= 20000, +2-3% at W = 5000,
+    // 4-30% slower when a worker has thousands of row blocks (W <= 1000 at
+    // 2^28 items; profiles/r01/deinterleave_tile_order.jsonl).
+    TransposeArgs b = a;
+    b.order = nrb <= 4 * grid ? 1u : 0u;
+    k_transpose<T, ROWS, BYTES><<<static_cast<unsigned>(grid), 256, smem, s>>>(b);
     return counted(cudaGetLastError());
 }
 

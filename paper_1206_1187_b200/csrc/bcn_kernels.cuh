@@ -136,6 +136,7 @@ struct TransposeArgs {
     uint64_t wpw;
     uint64_t i_base;  // element offset of the region inside each worker
     uint32_t itemsize;
+    uint32_t order;   // wide tiles: 0 = worker blocks vary fastest, 1 = row blocks
 };
 
 // Launchers (bcn_kernels.cu). Each returns the launch error, if any.

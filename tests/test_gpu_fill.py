@@ -111,13 +111,14 @@ def test_worker_and_layout_invariance(bcn, cuda, oracle, reference, workers):
 def test_deinterleave_shapes(bcn, cuda, oracle, itemsize):
     """Device deinterleave (parallel.cpp:81-97) of arbitrary words against the
     oracle: narrow (W <= 32, smem row tiles incl. exact tiles W | 8192) and wide
-    (64-row x 512-byte tiles, partial in both directions) regions, ragged
-    Interleaved tails, n smaller than W."""
+    (128-row tiles of 256 B to 1 KiB, partial in both directions, both tile
+    orders) regions, ragged Interleaved tails, n smaller than W."""
     rng = np.random.default_rng(itemsize)
     dt = np.uint32 if itemsize == 4 else np.uint64
     for n, w in [(1, 1), (5, 9), (100003, 1), (100003, 5), (100003, 7), (65536, 8), (100003, 31),
                  (100003, 32), (100003, 33), (100003, 63), (100003, 64), (100003, 65),
-                 (100003, 129), (300007, 1000), (99999, 99999), (2**21 + 17, 4099)]:
+                 (100003, 129), (300007, 1000), (99999, 99999), (2**21 + 17, 4099),
+                 (2**27 + 3, 130)]:  # thousands of row blocks per worker: worker-block tile order
         phys = rng.integers(0, np.iinfo(dt).max, n, dtype=dt, endpoint=True)
         plan = bcn.par.make_plan(n, w, bcn.Layout.Interleaved)
         signed = np.int32 if itemsize == 4 else np.int64
