@@ -128,6 +128,27 @@ def test_deinterleave_shapes(bcn, cuda, oracle, itemsize):
         assert np.array_equal(got, want), (n, w)
 
 
+def test_randomized_deinterleave_against_oracle(bcn, cuda, oracle):
+    """Seeded fuzz over the device deinterleave: random n, W (1 .. 2*10^6,
+    log-uniform, n < W included), item size and misaligned device views —
+    every narrow/wide tile shape, both wide tile orders and the ragged second
+    region, each bit-exact against the oracle's reordering."""
+    rng = np.random.default_rng(0xDE1_4721)
+    for case in range(120):
+        n = int(rng.integers(1, 3_000_000))
+        w = int(np.exp(rng.uniform(0, np.log(2e6))))
+        itemsize = int(rng.choice([4, 8]))
+        dt, sdt = (np.uint32, np.int32) if itemsize == 4 else (np.uint64, np.int64)
+        off = int(rng.integers(0, 3))
+        phys = rng.integers(0, np.iinfo(dt).max, n, dtype=dt, endpoint=True)
+        buf = torch.empty(n + off, dtype=torch.int32 if itemsize == 4 else torch.int64, device=cuda)
+        view = buf[off:]
+        view.copy_(torch.from_numpy(phys.view(sdt)))
+        plan = bcn.par.make_plan(n, w, bcn.Layout.Interleaved)
+        got = bcn.par.deinterleave(view, plan).cpu().numpy().view(dt)
+        assert np.array_equal(got, oracle.deinterleave(phys, w)), (case, n, w, itemsize, off)
+
+
 def test_interleaved_ragged_million(bcn, cuda, reference):
     """test_parallel.cpp:98-105: W = 7, n = 10^6, Interleaved."""
     got = dev_fill(bcn, 10**6, O.FMT_F64, workers=7, layout=1)
