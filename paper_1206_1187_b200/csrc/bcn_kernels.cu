@@ -1244,7 +1244,9 @@ cudaError_t transpose_t(const TransposeArgs& a, cudaStream_t s) {
         // the last tile column would be mostly empty (e.g. W = 129).
         // 4-byte items likewise fall back from 512-byte (128-worker) to
         // 256-byte (64-worker) tiles when the last tile column would be mostly
-        // empty (u32 W = 129: 0.54 ms with 128-worker tiles).
+        // empty (u32 W = 129: 0.54 ms with 128-worker tiles). 256-row u32
+        // tiles (1 KiB output runs) measured no better
+        // (profiles/r01/deinterleave_u32_256row_negative.jsonl).
         const uint64_t cover128 = (a.width + 127) / 128 * 128, cover64 = (a.width + 63) / 64 * 64;
         const bool wide_cols = cover128 * 10 <= cover64 * 11;
         if constexpr (sizeof(T) == 8) {
