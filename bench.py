@@ -129,9 +129,11 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ reference arm
-def reference_rate(n_sample: int, threads: int, reps: int = 1) -> tuple[float, float]:
-    """Time the reference's par::fill (oracle/_ref) on `threads` workers; returns
-    (variates/s, seconds per rep)."""
+def reference_rate(n_sample: int, threads: int, reps: int = 1,
+                   min_seconds: float = 0.0) -> tuple[float, float, int]:
+    """Time the reference's par::fill (oracle/_ref) on `threads` workers over
+    consecutive windows of the stream: at least `reps` calls and at least
+    `min_seconds` of wall time. Returns (variates/s, seconds per call, calls)."""
     import numpy as np
 
     import oracle as O
@@ -140,10 +142,12 @@ def reference_rate(n_sample: int, threads: int, reps: int = 1) -> tuple[float, f
     out = np.empty(n_sample, dtype=np.float64)
     ref.fill(n_sample, O.FMT_F64, workers=threads, out=out)  # warm pages
     t0 = time.perf_counter()
-    for r in range(reps):
+    r = 0
+    while r < reps or time.perf_counter() - t0 < min_seconds:
         ref.fill(n_sample, O.FMT_F64, workers=threads, base_offset=r * n_sample, out=out)
-    dt = (time.perf_counter() - t0) / reps
-    return n_sample / dt, dt
+        r += 1
+    dt = (time.perf_counter() - t0) / r
+    return n_sample / dt, dt, r
 
 
 def run_reference(args) -> None:
@@ -152,7 +156,7 @@ def run_reference(args) -> None:
         return
     threads = os.cpu_count() or 1
     # Calibrate, then size each step so the whole K+W run stays near a minute.
-    rate, _ = reference_rate(1 << 22, threads)
+    rate, _, _ = reference_rate(1 << 22, threads)
     budget_s = 60.0 / max(1, args.steps + args.warmup)
     n_step = 1 << 20
     while n_step < (1 << args.log2n) and (2 * n_step) / rate <= budget_s:
@@ -408,15 +412,19 @@ def main() -> None:
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
-        n_cpu = 1 << 27
-        rate, secs = reference_rate(n_cpu, threads)
+        # Bounded sample of the C2 workload: consecutive 2^27-double windows of
+        # the stream for >= 10 s of wall time on every host thread.
+        rate, secs, calls = reference_rate(1 << 27, threads, min_seconds=10.0)
         cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
                "sample": f"reference par::fill (oracle/_ref = unmodified /root/reference sources, "
-                         f"g++ -O3) of 2^27 doubles, W={threads} threads, {secs:.2f} s"}
-        # the single-thread rate too (config 1 = 10^6 doubles).
-        rate1, secs1 = reference_rate(10**6, 1, reps=5)
+                         f"g++ -O3): {calls} consecutive windows of 2^27 doubles of the C2 stream, "
+                         f"W={threads} threads, {calls * secs:.2f} s wall"}
+        # the single-thread rate too (config 1 = 10^6 doubles,
+        # repeated over consecutive windows for >= 2 s).
+        rate1, secs1, calls1 = reference_rate(10**6, 1, reps=5, min_seconds=2.0)
         cpu["single_thread"] = {"value": rate1, "unit": UNIT, "cores": 1,
-                                "sample": f"config 1: par::fill of 10^6 doubles, W=1, {secs1 * 1e3:.1f} ms"}
+                                "sample": f"config 1 windows: {calls1} x par::fill of 10^6 doubles, W=1, "
+                                          f"{calls1 * secs1:.2f} s"}
 
     ab_rows = run_ab(B, torch, dev, stream, timed, buf, fmt, args.ab) if args.ab else []
     sweep_rows = run_sweep(B, dev, stream, timed) if args.sweep else []

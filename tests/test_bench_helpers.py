@@ -69,3 +69,15 @@ def test_reference_arm_line_is_complete():
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
     assert line["cpu_baseline"]["kind"] == "reference" and line["cpu_baseline"]["cores"] >= 1
+
+
+def test_cpu_baseline_sample_is_time_bounded():
+    """cpu_baseline times consecutive windows of the stream until a minimum
+    wall time has passed (the 10 s sample of the bench line), and at least
+    `reps` calls."""
+    if not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libbcnref.so")):
+        pytest.skip("oracle/_ref not built")
+    rate, secs, calls = bench.reference_rate(1 << 16, 2, min_seconds=0.2)
+    assert rate > 0 and calls * secs >= 0.2
+    rate, secs, calls = bench.reference_rate(1 << 10, 1, reps=3)
+    assert calls >= 3
