@@ -69,7 +69,8 @@ inline CheckResult evaluate(const Check& c) {
 }
 
 // All four step kernels (with table `c`) agree with the exact 128-bit
-// reduction on the smallest and largest residues and on random ones.
+// reduction on the smallest and largest residues and on random ones, and so
+// do the four GPU jump engines (bcn_engine_check) on the random sample.
 inline Outcome kernels_agree(bool fast, const modred::ReductionConstants& c) {
     const std::uint64_t edge = fast ? 4096 : 65536, randoms = fast ? (1u << 16) : (1u << 20);
     auto agree = [&c](std::uint64_t v) {
@@ -81,9 +82,21 @@ inline Outcome kernels_agree(bool fast, const modred::ReductionConstants& c) {
     for (std::uint64_t d = 1; d <= edge; ++d)
         if (!agree(d) || !agree(modred::kModulus - d)) return {false, "mismatch near 0 or m"};
     Sampler rng(0xB200'5E1F'0001ull);
-    for (std::uint64_t t = 0; t < randoms; ++t)
-        if (!agree(rng.in(1, modred::kModulus - 1))) return {false, "mismatch on a random residue"};
-    return {true, std::to_string(2 * edge + randoms) + " residues, 4 kernels"};
+    std::vector<std::uint64_t> sample(randoms);
+    for (auto& v : sample) {
+        v = rng.in(1, modred::kModulus - 1);
+        if (!agree(v)) return {false, "mismatch on a random residue"};
+    }
+    // The GPU's jump engines, multiplier 2^53 mod m (one step), on the same sample.
+    const std::vector<std::uint64_t> step(randoms, modred::reduce_ref(Residue{1}).value);
+    std::vector<std::uint64_t> got(randoms);
+    for (bcn_engine e : {BCN_ENGINE_BARRETT, BCN_ENGINE_MONTGOMERY, BCN_ENGINE_FP64, BCN_ENGINE_MIXED}) {
+        b200::check(bcn_engine_check(e, sample.data(), step.data(), got.data(), randoms, 1, -1));
+        for (std::uint64_t i = 0; i < randoms; ++i)
+            if (got[i] != modred::reduce_ref(Residue{sample[i]}).value)
+                return {false, std::string("device engine ") + bcn_engine_name(e) + " disagrees"};
+    }
+    return {true, std::to_string(2 * edge + randoms) + " residues, 4 host kernels + 4 device engines"};
 }
 
 // state_at(a, k) = state_at(a, j) followed by k - j next() calls; the first

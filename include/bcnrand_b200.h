@@ -136,6 +136,15 @@ bcn_status bcn_seed_states(const uint64_t* a, const uint64_t* k, uint64_t* out, 
 bcn_status bcn_digest(const void* buf, uint64_t n, uint32_t itemsize, uint64_t index_base,
                       uint64_t d[3], int device, void* stream);
 
+/* Engine self-check (the device counterpart of the reference's kernel
+ * equivalence check, modred.hpp:103-159 / test_modred.cpp:73-96):
+ * out[i] = z[i] * c[i]^chain mod 3^33 computed by one jump engine (BARRETT,
+ * MONTGOMERY, FP64 or MIXED), the state kept in the engine's own
+ * representation between the `chain` multiplications. z[i] and c[i] in
+ * [0, 3^33); host arrays of `count` <= 2^26 items. Synchronous. */
+bcn_status bcn_engine_check(bcn_engine engine, const uint64_t* z, const uint64_t* c, uint64_t* out,
+                            uint64_t count, uint32_t chain, int device);
+
 /* The Constant writer (reference bench.cpp:60-63): identical geometry and
  * 256-bit stores as the contiguous fill, writing one fixed 8-byte pattern.
  * Device pointer, 32-byte aligned, nbytes a multiple of 1024. Asynchronous on

@@ -50,6 +50,7 @@ SIGNATURES = [
     ("bcn_digest", _int, [_vp, _u64, _u32, _u64, _pu64, _int, _vp]),
     ("bcn_fill_constant", _int, [_vp, _u64, _u64, _int, _vp]),
     ("bcn_fill_noise", _int, [_vp, _u64, _u64, _int, _vp]),
+    ("bcn_engine_check", _int, [_int, _vp, _vp, _vp, _u64, _u32, _int]),
     ("bcn_bench_fill", _int, [_u64, ctypes.c_uint32, _int, _u64, _int, _int, _int, _int,
                               ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
     ("bcn_format_text", _int, [_vp, _u64, _vp, _u64, _pu64]),

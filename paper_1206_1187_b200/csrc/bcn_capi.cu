@@ -1235,6 +1235,45 @@ bcn_status bcn_digest(const void* buf, uint64_t n, uint32_t itemsize, uint64_t i
     return BCN_OK;
 }
 
+bcn_status bcn_engine_check(bcn_engine engine, const uint64_t* z, const uint64_t* c, uint64_t* out,
+                            uint64_t count, uint32_t chain, int device) {
+    DeviceGuard guard;
+    if (engine != BCN_ENGINE_BARRETT && engine != BCN_ENGINE_MONTGOMERY && engine != BCN_ENGINE_FP64 &&
+        engine != BCN_ENGINE_MIXED)
+        return fail(BCN_ERR_INVALID_ARGUMENT, "engine_check: not a jump engine");
+    if (!z || !c || !out) return fail(BCN_ERR_INVALID_ARGUMENT, "engine_check: null buffer");
+    if (count > (1ull << 26)) return fail(BCN_ERR_INVALID_ARGUMENT, "engine_check: count above 2^26");
+    std::vector<Mult> mults(count);
+    for (uint64_t i = 0; i < count; ++i) {
+        if (z[i] >= kModulus || c[i] >= kModulus)
+            return fail(BCN_ERR_DOMAIN, "engine_check: residue or multiplier out of range");
+        mults[i] = host_make_mult(c[i]);
+    }
+    if (count == 0) return BCN_OK;
+    DevCtx* ctx = nullptr;
+    bcn_status st = get_ctx(device < 0 ? 0 : device, &ctx);
+    if (st) return st;
+    struct Buffers {
+        void* p = nullptr;
+        ~Buffers() {
+            if (p) cudaFree(p);
+        }
+    } b;
+    const size_t zb = count * 8, mb = count * sizeof(Mult);
+    BCN_CUDA(cudaMalloc(&b.p, 2 * zb + mb));
+    auto* dz = static_cast<uint64_t*>(b.p);
+    auto* dout = dz + count;
+    auto* dm = reinterpret_cast<Mult*>(dout + count);  // 16-byte aligned: 2 * count * 8 bytes in
+    const cudaStream_t s = ctx->stream;
+    BCN_CUDA(cudaMemcpyAsync(dz, z, zb, cudaMemcpyHostToDevice, s));
+    BCN_CUDA(cudaMemcpyAsync(dm, mults.data(), mb, cudaMemcpyHostToDevice, s));
+    cudaError_t e = launch_engine_check(engine, dz, dm, dout, count, chain, s);
+    if (e != cudaSuccess) return cuda_fail(e, "engine_check launch");
+    BCN_CUDA(cudaMemcpyAsync(out, dout, zb, cudaMemcpyDeviceToHost, s));
+    BCN_CUDA(cudaStreamSynchronize(s));
+    return BCN_OK;
+}
+
 namespace {
 // The Constant writer and its noise variant (bcn_fill_constant / bcn_fill_noise).
 bcn_status constant_writer(const char* what, void* out, uint64_t nbytes, uint64_t pattern,

@@ -775,6 +775,22 @@ __device__ __forceinline__ void digest_t(const DigestArgs& a, unsigned long long
     }
 }
 
+// Engine self-check: out[i] = z[i] * c[i]^chain mod m through one jump
+// engine, intermediate states kept in the engine's own (possibly balanced,
+// non-canonical) representation — exactness over the engine's whole reachable
+// domain, independent of the multipliers a fill happens to use.
+template <int ENG>
+__global__ void __launch_bounds__(256) k_engine_check(const uint64_t* z, const Mult* mult, uint64_t* out,
+                                                      uint64_t n, uint32_t chain) {
+    using E = Eng<ENG>;
+    for (uint64_t i = blockIdx.x * 256ull + threadIdx.x; i < n; i += gridDim.x * 256ull) {
+        const Mult k = mult[i];
+        typename E::State st = E::from_canonical(z[i]);
+        for (uint32_t r = 0; r < chain; ++r) st = E::mul(st, k);
+        out[i] = E::raw(st);
+    }
+}
+
 __global__ void __launch_bounds__(256) k_digest(const DigestArgs a) {
     unsigned long long s = 0, ws = 0, x = 0;
     if (a.itemsize == 8)
@@ -1189,6 +1205,20 @@ int bulk_blocks_per_sm(int fmt) {
 cudaError_t launch_seed(const SeedArgs& a, cudaStream_t s) {
     if (a.count == 0) return cudaSuccess;
     k_seed<<<static_cast<unsigned>((a.count + 255) / 256), 256, 0, s>>>(a);
+    return counted(cudaGetLastError());
+}
+
+cudaError_t launch_engine_check(int engine, const uint64_t* z, const Mult* mult, uint64_t* out, uint64_t n,
+                                uint32_t chain, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, 148ull * 16));
+    switch (engine) {
+        case kEngBarrett: k_engine_check<kEngBarrett><<<grid, 256, 0, s>>>(z, mult, out, n, chain); break;
+        case kEngMontgomery: k_engine_check<kEngMontgomery><<<grid, 256, 0, s>>>(z, mult, out, n, chain); break;
+        case kEngFP64: k_engine_check<kEngFP64><<<grid, 256, 0, s>>>(z, mult, out, n, chain); break;
+        case kEngMixed: k_engine_check<kEngMixed><<<grid, 256, 0, s>>>(z, mult, out, n, chain); break;
+        default: return cudaErrorInvalidValue;
+    }
     return counted(cudaGetLastError());
 }
 

@@ -151,6 +151,8 @@ cudaError_t launch_staged(int fmt, const StagedArgs& a, int grid, cudaStream_t s
 cudaError_t launch_bulk(int fmt, const ContigArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_seed(const SeedArgs& a, cudaStream_t s);
 cudaError_t launch_digest(const DigestArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_engine_check(int engine, const uint64_t* z, const Mult* mult, uint64_t* out, uint64_t n,
+                                uint32_t chain, cudaStream_t s);
 cudaError_t launch_constant(const ConstArgs& a, int grid, int block, cudaStream_t s);
 cudaError_t launch_transpose(const TransposeArgs& a, cudaStream_t s);
 

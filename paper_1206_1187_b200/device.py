@@ -45,6 +45,22 @@ def seed_states(a: torch.Tensor, k: torch.Tensor, steps: int = 0, stream=None) -
     return out
 
 
+def engine_check(engine: Engine, z, c, chain: int = 1, device: int = 0):
+    """z[i] * c[i]^chain mod 3^33 through one jump engine on the GPU
+    (bcn_engine_check): a self-check of the engine arithmetic over arbitrary
+    residues and multipliers. z, c: uint64 numpy arrays; returns uint64."""
+    import numpy as np
+
+    z = np.ascontiguousarray(z, dtype=np.uint64)
+    c = np.ascontiguousarray(c, dtype=np.uint64)
+    if z.shape != c.shape:
+        raise InvalidArgument("engine_check: z and c must have the same shape")
+    out = np.empty_like(z)
+    _lib.call("bcn_engine_check", int(engine), ctypes.c_void_p(z.ctypes.data), ctypes.c_void_p(c.ctypes.data),
+              ctypes.c_void_p(out.ctypes.data), z.size, chain, device)
+    return out
+
+
 def digest(buf: torch.Tensor, index_base: int = 0, stream=None) -> tuple[int, int, int]:
     """(sum x, sum (index_base+i+1) x, xor x (2(index_base+i)+1)) mod 2^64 over
     the raw 4- or 8-byte items of a CUDA tensor."""

@@ -28,7 +28,7 @@ def test_header_declares_the_boundary():
     syms = declared_symbols()
     for s in ("bcn_fill", "bcn_seed_from_index", "bcn_state_at", "bcn_next", "bcn_make_plan",
               "bcn_physical_index", "bcn_deinterleave", "bcn_seed_states", "bcn_fill_multi",
-              "bcn_digest", "bcn_fill_constant", "bcn_fill_noise", "bcn_last_error"):
+              "bcn_digest", "bcn_fill_constant", "bcn_fill_noise", "bcn_engine_check", "bcn_last_error"):
         assert s in syms
 
 

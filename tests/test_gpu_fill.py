@@ -520,6 +520,35 @@ def test_host_deinterleave_releases_its_staging(bcn, cuda, oracle):
     assert abs(torch.cuda.mem_get_info(cuda)[0] - free0) < (4 << 20)
 
 
+def test_jump_engines_exact_on_arbitrary_operands(bcn, cuda):
+    """Every jump engine (Barrett/Shoup, Montgomery, the FP64 error-free
+    product, Mixed) computes z * c^r mod 3^33 exactly for arbitrary residues
+    and multipliers — edges (0, 1, m/2, m/2 + 1, m - 1, 2^52 neighbourhoods)
+    and random ones — with r chained multiplications in the engine's own
+    (balanced, non-canonical) state representation, against Python integers.
+    This pins the DESIGN.md §2 exactness arguments over the engines' whole
+    domain, not just the multipliers the fills use."""
+    m = O.MODULUS
+    rng = np.random.default_rng(0xE9_1E5)
+    edges = [0, 1, 2, 3, m // 2 - 1, m // 2, m // 2 + 1, m - 2, m - 1, (1 << 52) - 1, 1 << 52,
+             (1 << 52) + 1, m - (1 << 51), 3 ** 32, 2 * 3 ** 32]
+    ze, ce = np.meshgrid(np.array(edges, dtype=np.uint64), np.array(edges, dtype=np.uint64))
+    n_rand = 1 << 17
+    z = np.concatenate([ze.ravel(), rng.integers(0, m, n_rand, dtype=np.uint64)])
+    c = np.concatenate([ce.ravel(), rng.integers(0, m, n_rand, dtype=np.uint64)])
+    zi, ci = [int(v) for v in z], [int(v) for v in c]
+    for chain in (1, 2, 7):
+        want = np.array([a * pow(b, chain, m) % m for a, b in zip(zi, ci)], dtype=np.uint64)
+        for engine in (bcn.Engine.Barrett, bcn.Engine.Montgomery, bcn.Engine.FP64, bcn.Engine.Mixed):
+            got = bcn.device.engine_check(engine, z, c, chain)
+            bad = np.nonzero(got != want)[0]
+            assert bad.size == 0, (engine, chain, [(zi[i], ci[i]) for i in bad[:5]])
+    with pytest.raises(bcn.DomainError):
+        bcn.device.engine_check(bcn.Engine.FP64, np.array([m], dtype=np.uint64), np.array([1], dtype=np.uint64))
+    with pytest.raises(bcn.InvalidArgument):
+        bcn.device.engine_check(bcn.Engine.Staged, z[:4], c[:4])
+
+
 def test_scalar_generator_api(bcn, cuda, oracle):
     g = bcn.gen
     s = g.seed_from_index(A0)
