@@ -1,6 +1,10 @@
 # Scratch driver for one gpurun call (edited per experiment).
 set -x
-mkdir -p gpurun_out/e2e
-for r in 1 2; do for mb in 16 32 64 128 256 512; do
-  BCN_HOST_CHUNK_MB=$mb timeout 300 python tools/e2e_chunk.py >> gpurun_out/e2e/chunk.jsonl 2>>gpurun_out/e2e/err.log
-done; done
+F=gpurun_out/san
+mkdir -p $F
+timeout 120 python tools/sanitize.py > $F/plain.log 2>&1
+for tool in memcheck racecheck; do
+  echo "## $tool" >> $F/san.txt
+  timeout 1200 /usr/local/cuda/bin/compute-sanitizer --tool $tool python tools/sanitize.py 2>&1 | grep -v "^========= *$" | tail -6 >> $F/san.txt
+  echo "exit=${PIPESTATUS[0]}" >> $F/san.txt
+done

@@ -64,6 +64,19 @@ def main() -> None:
         p = B.par.make_plan(20000, w, B.Layout.Interleaved)
         for dt in (torch.float64, torch.float32):
             B.par.deinterleave(torch.empty(20000, dtype=dt, device=dev).fill_(1), p)
+    # every transpose variant: 16-row narrow tiles (W = 100), 64-worker u32
+    # tiles (W = 129), both wide tile orders (W = 300 / 5000 at 400003 items)
+    rng = np.random.default_rng(5)
+    for n2, w in ((400003, 100), (400003, 129), (400003, 300), (400003, 5000), (3_000_017, 300)):
+        for npt, tdt in ((np.uint64, torch.int64), (np.uint32, torch.int32)):
+            phys = rng.integers(0, np.iinfo(npt).max, n2, dtype=npt, endpoint=True)
+            src = torch.from_numpy(phys.view(np.int64 if npt == np.uint64 else np.int32)).to(dev)
+            got = B.par.deinterleave(src, B.par.make_plan(n2, w, B.Layout.Interleaved)).cpu().numpy()
+            assert np.array_equal(got.view(npt), o.deinterleave(phys, w)), (n2, w, npt)
+    zz = rng.integers(0, O.MODULUS, 4096, dtype=np.uint64)
+    cc = rng.integers(0, O.MODULUS, 4096, dtype=np.uint64)
+    for eng in (B.Engine.Barrett, B.Engine.Montgomery, B.Engine.FP64, B.Engine.Mixed):
+        B.device.engine_check(eng, zz, cc, 3)
     torch.cuda.synchronize()
     print("sanitize workload ok")
 
