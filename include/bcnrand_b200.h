@@ -77,6 +77,9 @@ const char* bcn_engine_name(int engine);
 /* Number of visible CUDA devices (0 when none; never an error). */
 int bcn_device_count(void);
 
+/* L2 cache size of `device` in bytes (0 when there is no such device). */
+uint64_t bcn_l2_bytes(int device);
+
 /* ---- generator.hpp ------------------------------------------------------ */
 /* generator.hpp:33 / generator.cpp:17-30 — 2^e mod `modulus` (odd, < 2^63). */
 bcn_status bcn_modpow2(uint64_t e, uint64_t modulus, uint64_t* out);

@@ -28,6 +28,7 @@ SIGNATURES = [
     ("bcn_last_error", ctypes.c_char_p, []),
     ("bcn_engine_name", ctypes.c_char_p, [_int]),
     ("bcn_device_count", _int, []),
+    ("bcn_l2_bytes", _u64, [_int]),
     ("bcn_auto_engine", _int, [_int]),
     ("bcn_launch_count", _u64, []),
     ("bcn_set_launch_config", _int, [_int, _int]),

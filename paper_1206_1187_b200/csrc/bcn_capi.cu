@@ -853,6 +853,15 @@ const char* bcn_engine_name(int engine) {
     return "?";
 }
 
+uint64_t bcn_l2_bytes(int device) {
+    int bytes = 0;
+    if (cudaDeviceGetAttribute(&bytes, cudaDevAttrL2CacheSize, device < 0 ? 0 : device) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return static_cast<uint64_t>(bytes);
+}
+
 int bcn_device_count(void) {
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess) {

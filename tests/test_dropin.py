@@ -3,9 +3,9 @@ ABI. Two programs written against those headers are built by tests/cpp/Makefile:
 
 * tests/cpp/build/test_dropin — this repo's C++ tests of the drop-in;
 * oracle/_ref/ref_tests_on_b200 — the REFERENCE's own unit tests
-  (tests/test_{generator,parallel,quality,selftest,bench}.cpp, unmodified, compiled
-  in place from /root/reference) linked against libbcnrand_b200.so, i.e. the
-  reference's test suite for this path running on the B200 library (GPU);
+  (tests/test_{generator,parallel,quality,selftest,bench,cli}.cpp, unmodified,
+  compiled in place from /root/reference) linked against libbcnrand_b200.so,
+  i.e. the reference's test suite running on the B200 library (GPU);
 * oracle/_ref/ref_host_tests — its tests/test_{modred,oracle}.cpp against the
   host-only parts of the drop-in (CPU suite).
 """
@@ -105,6 +105,55 @@ def _run(path: str) -> str:
     return out
 
 
+CLI = os.path.join(ROOT, "tests", "cpp", "build", "bcnrand")
+
+
+def test_cli_executable_usage_paths():
+    """The `bcnrand` executable (include/bcnrand/cli.hpp, tools/bcnrand_main.cpp):
+    the paths that need no GPU — seed-info and the usage / I/O exit codes of
+    the reference (cli.cpp:24-27, test_cli.cpp:127-143)."""
+    r = subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp"), "cli"],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+
+    def run(*args):
+        return subprocess.run([CLI, *args], capture_output=True, text=True, timeout=60)
+
+    r = run("seed-info", "5559060566555623")
+    assert r.returncode == 0 and "z0             = 4258649398211344" in r.stdout
+    assert "z0 * 3^-33     = 0.76607357434316758" in r.stdout
+    assert run("seed-info", "5559060566555622").returncode == 2
+    assert run("seed-info", "9007199254740992").returncode == 0
+    assert run("seed-info", "9007199254740993").returncode == 2
+    assert run("gen", "--n", "5", "--seed", "100").returncode == 2
+    assert run("gen", "--n", "5", "--format", "xml").returncode == 2
+    assert run("gen").returncode == 2
+    assert run("frobnicate").returncode == 2
+    assert run("gen", "--n", "5", "--out", "/nonexistent-dir/x").returncode == 3
+    assert run("gen", "--n", "5", "--bogus", "1").returncode == 2
+    assert run("--help").returncode == 0
+
+
+@pytest.mark.gpu
+def test_cli_executable_generates(cuda, tmp_path):
+    """`bcnrand gen` on the GPU: raw-u64 n=1 is the golden z1, raw-f64 bytes are
+    identical for W = 1 / 8 / 8 interleaved and chunked streaming, and
+    `selftest --fast` passes."""
+    if not os.path.exists(CLI):
+        pytest.skip("tests/cpp/build/bcnrand not built")
+    one = tmp_path / "one.u64"
+    assert subprocess.run([CLI, "gen", "--n", "1", "--format", "raw-u64", "--out", str(one)]).returncode == 0
+    assert int.from_bytes(one.read_bytes(), "little") == 2138759898642167
+    outs = []
+    for extra in ([], ["--workers", "8"], ["--workers", "8", "--layout", "interleaved"], ["--chunk", "7777"]):
+        f = tmp_path / f"u{len(outs)}.f64"
+        assert subprocess.run([CLI, "gen", "--n", "40000", "--format", "raw-f64", "--out", str(f), *extra]).returncode == 0
+        outs.append(f.read_bytes())
+    assert len(outs[0]) == 320000 and all(o == outs[0] for o in outs)
+    r = subprocess.run([CLI, "selftest", "--fast"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "selftest: all checks passed" in r.stdout, r.stdout + r.stderr
+
+
 @pytest.mark.gpu
 def test_cpp_dropin_suite(cuda):
     if not os.path.exists(DROPIN):
@@ -115,14 +164,16 @@ def test_cpp_dropin_suite(cuda):
 @pytest.mark.gpu
 def test_reference_unit_tests_pass_on_the_b200_library(cuda):
     """The reference's test_generator.cpp / test_parallel.cpp / test_quality.cpp /
-    test_selftest.cpp / test_bench.cpp (40 cases, ~3.5M assertions incl.
-    worker/layout invariance, base_offset windows, the built-in selftest with a
-    corrupted constant table and the throughput harness) pass when compiled
-    against the drop-in headers and run on the GPU."""
+    test_selftest.cpp / test_bench.cpp / test_cli.cpp (49 cases, ~3.5M
+    assertions incl. worker/layout invariance, base_offset windows, the
+    built-in selftest with a corrupted constant table, the throughput harness
+    and the `bcnrand` command line: byte formats, chunked == single-shot,
+    exit codes) pass when compiled against the drop-in headers and run on the
+    GPU."""
     if not os.path.exists(REFTESTS):
         pytest.skip("oracle/_ref/ref_tests_on_b200 not built (needs /root/reference at build time)")
     out = _run(REFTESTS)
-    assert "test cases: 40 | 40 passed | 0 failed" in out, out
+    assert "test cases: 49 | 49 passed | 0 failed" in out, out
 
 
 @pytest.mark.gpu
