@@ -425,6 +425,19 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
                 else
                     bits[h][v] = emit_bits<FMT, E>(st[h][v]);
             }
+        // Interleaved: this round's multiplier of every stream, loaded before
+        // the pacer barrier so the shared-memory latency overlaps the wait.
+        Mult sel[INTER ? H : 1][INTER ? V : 1];
+        if constexpr (INTER) {
+#pragma unroll
+            for (int h = 0; h < H; ++h)
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    const bool same = col[h][v] < same_below;
+                    sel[h][v] = jumps[same ? 0 : 1];
+                    col[h][v] += same ? adv_same : adv_wrap;
+                }
+        }
         asm volatile("bar.sync 1, %0;" ::"n"(kPacedThreads) : "memory");
         if (r + H <= count) {
 #pragma unroll
@@ -438,11 +451,7 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
 #pragma unroll
             for (int h = 0; h < H; ++h)
 #pragma unroll
-                for (int v = 0; v < V; ++v) {
-                    const bool same = col[h][v] < same_below;
-                    st[h][v] = E::mul(st[h][v], jumps[same ? 0 : 1]);
-                    col[h][v] += same ? adv_same : adv_wrap;
-                }
+                for (int v = 0; v < V; ++v) st[h][v] = E::mul(st[h][v], sel[h][v]);
         } else if constexpr (!CONST) {
 #pragma unroll
             for (int h = 0; h < H; ++h)
