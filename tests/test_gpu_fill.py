@@ -5,6 +5,7 @@ reference, bit-exact. Mirrors the reference's own tests
 from __future__ import annotations
 
 import hashlib
+import os
 
 import numpy as np
 import pytest
@@ -134,7 +135,7 @@ def test_randomized_deinterleave_against_oracle(bcn, cuda, oracle):
     every narrow/wide tile shape, both wide tile orders and the ragged second
     region, each bit-exact against the oracle's reordering."""
     rng = np.random.default_rng(0xDE1_4721)
-    for case in range(120):
+    for case in range(int(os.environ.get("BCN_FUZZ_CASES_DEINT", "120"))):
         n = int(rng.integers(1, 3_000_000))
         w = int(np.exp(rng.uniform(0, np.log(2e6))))
         itemsize = int(rng.choice([4, 8]))
@@ -201,7 +202,7 @@ def test_randomized_plans_against_oracle(bcn, cuda, oracle):
     rng = np.random.default_rng(0x1206_1187)
     P = 3706040377703682
     engines = ["Auto", "Barrett", "Montgomery", "FP64", "Staged", "Bulk", "Mixed"]
-    for case in range(400):
+    for case in range(int(os.environ.get("BCN_FUZZ_CASES", "400"))):
         n = int(rng.choice([rng.integers(1, 300), rng.integers(300, 5000), rng.integers(5000, 400000)]))
         workers = int(rng.choice([1, 2, 3, 5, 7, 8, 16, 31, 33, 64, 100, 1000, rng.integers(1, 5000)]))
         layout = int(rng.integers(0, 2))
