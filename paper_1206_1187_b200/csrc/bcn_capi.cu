@@ -436,8 +436,11 @@ cudaError_t enqueue_region(const FillJob& j, char* dptr, uint64_t slot0, uint64_
         // elements), as in the contiguous kernel. The grid must then be a
         // multiple of width / gcd(width, row * kWorkers * H): taken if such a
         // grid keeps >= 95% of the contiguous grid (W = 7: 147 CTAs, W = 64:
-        // 148) or >= 80% of a 2-CTA-per-SM grid (W = 1000: 250);
-        // profiles/r01/interleaved_fixed*.jsonl.
+        // 148), or, for W < 250, >= 80% of a 2-CTA-per-SM grid (W = 125: 250
+        // CTAs); profiles/r01/interleaved_fixed*.jsonl. From W = 250 the
+        // two-multiplier mode (multiplier loads hoisted above the pacer
+        // barrier) matches or beats the uneven 250-CTA grid (W = 250 / 1000 /
+        // 2000: +2 / +4 / +0-5%; interleaved_fixed_vs_two_mult.jsonl).
         const uint64_t per_cta = row * kWorkers * paced_rows_per_round(j.fmt);
         const uint64_t unit = width / std::gcd(width, per_cta);
         const uint64_t need = std::max<uint64_t>(1, (rows + kWorkers - 1) / kWorkers);
@@ -447,7 +450,7 @@ cudaError_t enqueue_region(const FillJob& j, char* dptr, uint64_t slot0, uint64_
             return g >= 1 && g * 100 >= base * pct ? g : 0;
         };
         uint64_t fixed_grid = fixed_for(paced_grid(j.ctx, engine), 95);
-        if (!fixed_grid) fixed_grid = fixed_for(2ull * j.ctx->sms, 80);
+        if (!fixed_grid && width < 250) fixed_grid = fixed_for(2ull * j.ctx->sms, 80);
         if (paced(j.fmt, engine) && fixed_grid) {
             const uint64_t S = per_cta * fixed_grid;
             PacedArgs pa{};
