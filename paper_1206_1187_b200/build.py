@@ -39,18 +39,28 @@ def stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile libbcnrand_b200.so if any input changed; return its path."""
+    """Compile libbcnrand_b200.so if any input changed; return its path.
+
+    Serialised by a file lock: several ranks of one job (torchrun) may call
+    this at once; the first rebuilds, the others find the library fresh."""
     if not force and not stale():
         return LIB
-    cmd = [NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC",
-           "-Xcompiler", "-O3", "-shared", "-cudart", "static",
-           "-I", os.path.join(ROOT, "include"),
-           "-o", LIB + ".tmp", *[os.path.join(CSRC, f) for f in SOURCES]]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.run(cmd, check=True)
-    os.replace(LIB + ".tmp", LIB)
+    import fcntl
+
+    with open(LIB + ".lock", "w") as lock:
+        fcntl.flock(lock, fcntl.LOCK_EX)
+        if not force and not stale():
+            return LIB
+        tmp = f"{LIB}.tmp{os.getpid()}"
+        cmd = [NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC",
+               "-Xcompiler", "-O3", "-shared", "-cudart", "static",
+               "-I", os.path.join(ROOT, "include"),
+               "-o", tmp, *[os.path.join(CSRC, f) for f in SOURCES]]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True)
+        os.replace(tmp, LIB)
     return LIB
 
 
