@@ -122,7 +122,10 @@ class ClockSampler:
             limit = self.nvml.nvmlDeviceGetEnforcedPowerLimit(self.h) / 1000.0 if self.nvml else None
         except Exception:  # noqa: BLE001
             pass
+        srt = sorted(self.samples)
         return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_mhz_mean": statistics.mean(self.samples) if self.samples else None,
+                "sm_mhz_p10": srt[len(srt) // 10] if srt else None,  # NVML's reading lags the power controller
                 "sm_max_mhz": self.max_mhz, "samples": len(self.samples), "reasons": names,
                 "power_w_median": statistics.median(self.power) if self.power else None,  # instantaneous
                 "power_limit_w": limit}
