@@ -19,6 +19,8 @@
 //                                 heads/tails, u64-wrap corner cases); one seed per slot.
 //   k_seed                        batched state_at / next walks (skip-ahead stress).
 //   k_digest                      order-sensitive checksums for verification.
+//   k_engine_check<ENG>           z * c^r mod m through one jump engine on arbitrary
+//                                 operands (bcn_engine_check, engine self-check).
 //   k_constant                    the unpaced Constant writer: identical access
 //                                 pattern, fixed value (the paper's memory ceiling).
 //   k_transpose, k_transpose_narrow
