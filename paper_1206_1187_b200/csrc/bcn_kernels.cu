@@ -1270,7 +1270,13 @@ cudaError_t transpose_t(const TransposeArgs& a, cudaStream_t s) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (a.width <= kNarrowMaxWidth) {
+    // Narrow row tiles up to W = 128 for 4-byte items; 8-byte items switch to
+    // the wide 128-worker (1 KiB) tiles from W = 86: one partly filled column
+    // block with 1 KiB output runs beats 80-112-row narrow tiles there
+    // (W = 100: 5.4 vs 4.9 TB/s, W = 120: 5.8 vs 4.8, W = 128: 5.85 vs 5.5;
+    // crossover at W ~ 86; profiles/r01/deinterleave_narrow_vs_wide.jsonl).
+    constexpr uint64_t narrow_max = sizeof(T) == 8 ? 85 : kNarrowMaxWidth;
+    if (a.width <= narrow_max) {
         using G = NarrowTile<T>;
         const size_t smem = (G::kItems + kNarrowMaxWidth) * sizeof(T);
         cudaFuncSetAttribute(k_transpose_narrow<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
