@@ -940,7 +940,8 @@ __global__ void __launch_bounds__(256) k_transpose(const TransposeArgs a) {
     }
 }
 
-// Narrow regions (width <= kNarrowMaxWidth workers): tiles of R whole rows
+// Narrow regions (width <= kNarrowMaxWidth workers for 4-byte items, <= 85
+// for 8-byte items; transpose_t): tiles of R whole rows
 // (R*width <= kNarrowItems slots, R a multiple of 64, or of 16 when W > 64) are one contiguous span
 // of the input, read fully coalesced (kNarrowItems/256 loads per thread),
 // scattered into shared memory as [width][R] with an odd pitch (row = slot /
