@@ -1,17 +1,13 @@
 # Scratch driver for one gpurun call (edited per experiment).
 set -x
-F=gpurun_out/final4
+F=gpurun_out/pitch
 mkdir -p $F
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit --format=csv > $F/gpu.txt
-timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -15 > $F/pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $F/smoke.log 2>&1
-oracle/_ref/ref_tests_on_b200 2>&1 | tail -2 > $F/ref_tests.log
-timeout 600 python bench.py --impl reference > $F/bench_reference.json 2> $F/bench_reference.err
-for i in 1 2 3; do timeout 600 python bench.py 2>>$F/bench.err >> $F/bench.jsonl; done
-for tool in memcheck racecheck; do
-  echo "## $tool" >> $F/san.txt
-  timeout 1200 /usr/local/cuda/bin/compute-sanitizer --tool $tool python tools/sanitize.py 2>&1 | grep -v "^========= *$" | tail -4 >> $F/san.txt
+L=paper_1206_1187_b200/libbcnrand_b200.so
+for r in 1 2; do
+  for v in old new; do
+    cp abtest/$v.so $L
+    timeout 300 python tools/deint_perf.py 2,3,5,7,9,12,16,24 | sed "s/^{/{\"variant\": \"$v\", \"rep\": $r, /" >> $F/ab.jsonl
+  done
 done
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $F/launches_bench.csv python bench.py --steps 20 --warmup 3 > $F/bench_under_ncu.log 2>&1
-timeout 1500 ncu --set full --clock-control none --import-source on -f -o /tmp/prof_all python tools/profile_all.py > $F/ncu_full.log 2>&1
-python tools/ncu_summary.py /tmp/prof_all.ncu-rep -o $F/ncu_full_all_kernels.json >> $F/ncu_full.log 2>&1
+cp abtest/new.so $L
+timeout 900 python -m pytest tests/test_gpu_fill.py -m gpu -q -k "deinterleave or interleaved" 2>&1 | tail -3 > $F/pytest.log
