@@ -126,6 +126,12 @@ def test_no_cpu_fallback_without_gpu(bcn):
     with pytest.raises(bcn.CudaError, match="no CUDA device"):
         bcn.par.fill(buf, bcn.par.make_plan(1000, 1), O.MIN_SEED)
     assert (buf == -1.0).all()  # nothing was computed on the host
+    # the other device-only entry points fail the same way (no host compute)
+    from paper_1206_1187_b200 import _lib
+
+    assert _lib.lib().bcn_l2_bytes(0) == 0 and _lib.lib().bcn_device_count() == 0
+    with pytest.raises(bcn.CudaError):
+        bcn.device.engine_check(bcn.Engine.FP64, np.array([5], dtype=np.uint64), np.array([7], dtype=np.uint64))
 
 
 def test_physical_index_and_plans_match_reference_semantics(bcn, oracle):
