@@ -1164,6 +1164,7 @@ bcn_status bcn_deinterleave(const void* in, void* out, uint64_t n, uint32_t work
     t.wpw = p.wpw;
     t.itemsize = itemsize;
     t.order = 0;  // chosen per region by the launcher
+    t.pitch = 0;
     // Region 1: rows [0, sc) of all workers; region 2: the remaining
     // wpw - sc elements of workers 0..W-2 (parallel.cpp:24-33). One
     // persistent-grid launch per region.

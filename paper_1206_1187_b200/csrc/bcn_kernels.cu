@@ -988,7 +988,7 @@ __global__ void __launch_bounds__(256) k_transpose_narrow(const TransposeArgs a)
     T* out = static_cast<T*>(a.out);
     const unsigned W = static_cast<unsigned>(a.width);
     const unsigned R = G::rows(W);  // rows per tile
-    const unsigned P = R | 1;                      // odd pitch
+    const unsigned P = a.pitch ? a.pitch : (R | 1);  // smem pitch (narrow_pitch)
     // slot / W == (slot * M) >> 32 exactly for slot < 2^32 / W, M = ceil(2^32 / W)
     const uint64_t M = ((1ull << 32) + W - 1) / W;
     const uint64_t ntiles = (a.rows + R - 1) / R;
@@ -1266,6 +1266,41 @@ cudaError_t transpose_wide(const TransposeArgs& a, int sms, cudaStream_t s) {
     return counted(cudaGetLastError());
 }
 
+// Shared-memory pitch of a narrow 4-byte tile: the scatter writes slot q of
+// the span to tile[(q % W) * P + q / W], so for W < 32 one warp touches
+// several tile rows and the default odd pitch R | 1 (== 1 mod 32 for R a
+// multiple of 64) puts (c, r) and (c + 1, r - 1) in one bank. Where that
+// costs >= 5-way conflicts on average (W = 5, 6, 7) take the pad (W * pad
+// within the kNarrowMaxWidth spare items) with the fewest conflicts over every
+// warp alignment: +11 / +20 / +18% there. Re-pitching milder cases measured
+// 1-6% slower (W = 3, 4, 8-16), so they keep R | 1
+// (profiles/r01/deinterleave_pitch_u32_abba.jsonl, ABBA order, 4 reps).
+unsigned narrow_conflicts_u32(unsigned W, unsigned P) {
+    unsigned cost = 0;
+    for (unsigned start = 0; start < W; ++start) {
+        unsigned count[32] = {}, worst = 0;
+        for (unsigned l = 0; l < 32; ++l) {
+            const unsigned q = start + l;
+            worst = std::max(worst, ++count[((q % W) * P + q / W) % 32]);
+        }
+        cost += worst;
+    }
+    return cost;  // summed over the W warp alignments
+}
+
+unsigned narrow_pitch_u32(unsigned W, unsigned R) {
+    if (W >= 32 || narrow_conflicts_u32(W, R | 1) < 5 * W) return R | 1;
+    unsigned best = R | 1, best_cost = ~0u;
+    for (unsigned pad = 1; pad * W <= kNarrowMaxWidth; ++pad) {
+        const unsigned cost = narrow_conflicts_u32(W, R + pad);
+        if (cost < best_cost) {
+            best_cost = cost;
+            best = R + pad;
+        }
+    }
+    return best;
+}
+
 template <typename T>
 cudaError_t transpose_t(const TransposeArgs& a, cudaStream_t s) {
     int dev = 0, sms = 148;
@@ -1285,7 +1320,9 @@ cudaError_t transpose_t(const TransposeArgs& a, cudaStream_t s) {
         const uint64_t rows_per_tile = G::rows(static_cast<unsigned>(a.width));
         const uint64_t tiles = (a.rows + rows_per_tile - 1) / rows_per_tile;
         const uint64_t cap = static_cast<uint64_t>(sms) * occupancy(k_transpose_narrow<T>, 256, smem);
-        k_transpose_narrow<T><<<static_cast<unsigned>(std::min(tiles, cap)), 256, smem, s>>>(a);
+        TransposeArgs b = a;
+        b.pitch = sizeof(T) == 4 ? narrow_pitch_u32(static_cast<unsigned>(a.width), static_cast<unsigned>(rows_per_tile)) : 0;
+        k_transpose_narrow<T><<<static_cast<unsigned>(std::min(tiles, cap)), 256, smem, s>>>(b);
     } else {
         // Tile shape sweep (profiles/r01/deinterleave_tiles.jsonl): 128-row
         // tiles win everywhere; 8-byte items prefer 1 KiB input runs unless

@@ -137,6 +137,7 @@ struct TransposeArgs {
     uint64_t i_base;  // element offset of the region inside each worker
     uint32_t itemsize;
     uint32_t order;   // wide tiles: 0 = worker blocks vary fastest, 1 = row blocks
+    uint32_t pitch;   // narrow tiles: smem row pitch in items (0 = rows | 1)
 };
 
 // Launchers (bcn_kernels.cu). Each returns the launch error, if any.
