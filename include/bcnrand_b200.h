@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define BCN_ABI_VERSION 1
+#define BCN_ABI_VERSION 2
 
 typedef enum bcn_status {
     BCN_OK = 0,
@@ -112,12 +112,15 @@ bcn_status bcn_fill(void* out, uint64_t capacity, uint64_t n, bcn_format format,
 
 /* Multi-GPU fill from one host process: the logical range [0, n) is split with
  * make_plan(n, ndev) (contiguous shards) and shard g is written to outs[g]
- * (device memory of devices[g], capacity >= shard size) with base_offset +
- * its start, one host thread and stream per device, no collective. The
- * concatenation of the shards is bit-identical to a single-device fill. */
-bcn_status bcn_fill_multi(void* const* outs, const int* devices, int ndev, uint64_t n,
-                          bcn_format format, uint64_t seed_index, uint64_t base_offset,
-                          bcn_engine engine);
+ * (device memory of devices[g], capacities[g] items, >= the shard size, else
+ * std::invalid_argument before any device work) with base_offset + its start,
+ * one host thread per device, no collective. streams: NULL (each device drains,
+ * then the library's stream) or one stream per shard (the caller orders).
+ * Synchronous. The concatenation of the shards is bit-identical to a
+ * single-device fill. */
+bcn_status bcn_fill_multi(void* const* outs, const uint64_t* capacities, const int* devices, int ndev,
+                          uint64_t n, bcn_format format, uint64_t seed_index, uint64_t base_offset,
+                          bcn_engine engine, void* const* streams);
 
 /* parallel.hpp:58-60 — de-interleave an Interleaved buffer of plan.n items
  * (itemsize 4 or 8) into logical order. Both pointers on `device` (or both
@@ -189,14 +192,31 @@ bcn_status bcn_set_launch_config(int ctas_per_sm, int row_order);
 
 /* Process-wide HBM write pacing of the contiguous fill and Constant kernels.
  * B200 write efficiency drops when SM stores oversubscribe HBM; the paced
- * kernels meter their stores to `target_gbs` (GB/s, per device) with one pacer
- * warp per CTA reading %globaltimer. 0 disables pacing. ctas_per_sm in [1,7]
- * (default 1: 8 worker warps per SM — measured ~1.3% faster sustained than 2);
- * format_mask: bit f enables pacing for bcn_format f (default U64|F64 = 3).
- * Output bits never depend on it. */
+ * kernels meter their stores to a target rate (GB/s, per device) with one pacer
+ * thread per CTA reading %globaltimer. target_gbs < 0: automatic (default) —
+ * each device uses the target its context measured at initialisation (a short
+ * sweep of the paced fill: the highest target it still holds within 2%, minus
+ * 100 GB/s; BCN_PACE_CALIBRATE=0 skips the sweep and uses 7200); 0: unpaced;
+ * otherwise a fixed target >= 100. ctas_per_sm in [1,7] (default 1: 8 worker
+ * warps per SM — measured ~1.3% faster sustained than 2); format_mask: bit f
+ * enables pacing for bcn_format f (default U64|F64 = 3). Output bits never
+ * depend on it. */
 bcn_status bcn_set_write_pacing(double target_gbs, int ctas_per_sm, int format_mask);
-/* Current pacing target in GB/s (0 = unpaced). */
+/* The pacing setting in GB/s (< 0 = automatic, 0 = unpaced). */
 double bcn_write_pacing(void);
+/* Where a device's effective pacing target comes from. */
+typedef enum bcn_pace_source {
+    BCN_PACE_UNPACED = 0,
+    BCN_PACE_USER = 1,        /* bcn_set_write_pacing with a fixed target   */
+    BCN_PACE_CALIBRATED = 2,  /* measured by this process on this device    */
+    BCN_PACE_DEFAULT = 3      /* calibration disabled or failed: 7200 GB/s  */
+} bcn_pace_source;
+/* Effective pacing target of `device` (0 = unpaced) and its source; runs the
+ * device's calibration first if it has not run yet. */
+bcn_status bcn_device_write_pacing(int device, double* target_gbs, int* source);
+/* The (target, achieved) GB/s points of `device`'s calibration sweep; *count
+ * = number of points (at most `capacity` are written). */
+bcn_status bcn_pace_calibration(int device, double* targets, double* achieved, int capacity, int* count);
 /* Current pacing configuration (any pointer may be NULL). */
 void bcn_get_write_pacing(double* target_gbs, int* ctas_per_sm, int* format_mask);
 

@@ -36,6 +36,9 @@ SIGNATURES = [
     ("bcn_get_write_pacing", None, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_int),
                                     ctypes.POINTER(_int)]),
     ("bcn_write_pacing", ctypes.c_double, []),
+    ("bcn_device_write_pacing", _int, [_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_int)]),
+    ("bcn_pace_calibration", _int, [_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
+                                    _int, ctypes.POINTER(_int)]),
     ("bcn_modpow2", _int, [_u64, _u64, _pu64]),
     ("bcn_seed_from_index", _int, [_u64, _pu64]),
     ("bcn_state_at", _int, [_u64, _u64, _pu64]),
@@ -44,8 +47,8 @@ SIGNATURES = [
     ("bcn_make_plan", _int, [_u64, _u32, ctypes.POINTER(_u32), _pu64]),
     ("bcn_physical_index", _int, [_u64, _u32, _int, _u32, _u64, _pu64]),
     ("bcn_fill", _int, [_vp, _u64, _u64, _int, _u32, _int, _u64, _int, _u64, _int, _int, _vp]),
-    ("bcn_fill_multi", _int, [ctypes.POINTER(_vp), ctypes.POINTER(_int), _int, _u64, _int, _u64,
-                              _u64, _int]),
+    ("bcn_fill_multi", _int, [ctypes.POINTER(_vp), _pu64, ctypes.POINTER(_int), _int, _u64, _int, _u64,
+                              _u64, _int, ctypes.POINTER(_vp)]),
     ("bcn_deinterleave", _int, [_vp, _vp, _u64, _u32, _u32, _int, _vp]),
     ("bcn_seed_states", _int, [_vp, _vp, _vp, _u64, _u32, _int, _vp]),
     ("bcn_digest", _int, [_vp, _u64, _u32, _u64, _pu64, _int, _vp]),

@@ -100,12 +100,21 @@ struct DevCtx {
     std::mutex occ_mu;                // guards occ
     std::mutex mu;                    // serialises host-buffer fills on this device
     std::mutex small_mu;              // serialises users of digest / flag / qscratch
+    // Automatic write pacing (calibrate_pace): this device's target and the
+    // sweep it came from.
+    std::once_flag pace_once;
+    double pace_cal = kDefaultPaceGBs;
+    int pace_src = BCN_PACE_DEFAULT;
+    std::vector<std::pair<double, double>> pace_curve;  // (target, achieved) GB/s
 };
 
 std::mutex g_ctx_mu;
 std::map<int, DevCtx*> g_ctx;
 
-bcn_status get_ctx(int device, DevCtx** out) {
+double pace_gbs(DevCtx* c);
+std::atomic<double>& pace_setting();
+
+bcn_status get_ctx_nocal(int device, DevCtx** out) {
     int count = 0;
     cudaError_t e = cudaGetDeviceCount(&count);
     if (e != cudaSuccess || count == 0)
@@ -128,6 +137,14 @@ bcn_status get_ctx(int device, DevCtx** out) {
     }
     *out = c;
     return BCN_OK;
+}
+
+bcn_status get_ctx(int device, DevCtx** out) {
+    bcn_status st = get_ctx_nocal(device, out);
+    // Automatic pacing: measure this device's target once, at context
+    // initialisation, so no fill (or timed region) pays for it later.
+    if (!st && pace_setting().load() < 0.0) pace_gbs(*out);
+    return st;
 }
 
 // Restores the calling thread's current device on scope exit: entry points
@@ -203,10 +220,13 @@ int blocks_per_sm(DevCtx* c, int fmt, int engine, bool interleaved) {
 std::atomic<int> g_ctas_per_sm{0};
 std::atomic<int> g_row_order{1};
 // Write pacing (bcn_set_write_pacing): target HBM write rate of the paced
-// contiguous kernels in GB/s (0 = unpaced) and their CTAs per SM.
-std::atomic<double> g_pace_gbs{kDefaultPaceGBs};
+// contiguous kernels in GB/s — < 0: automatic (each device's calibrated
+// target, calibrate_pace), 0: unpaced, else fixed — and their CTAs per SM.
+constexpr double kMinPaceGBs = 100.0;  // lower fixed targets would stall a launch for seconds
+std::atomic<double> g_pace_gbs{-1.0};
 std::atomic<int> g_pace_cps{kDefaultPaceCps};
 std::atomic<int> g_pace_formats{(1 << kFmtU64) | (1 << kFmtF64)};
+std::atomic<double>& pace_setting() { return g_pace_gbs; }
 
 // CTAs of the paced grid: ctas_per_sm x SMs, or BCN_PACE_GRID (an
 // exploration override: total CTAs, e.g. to leave SMs idle under a power cap).
@@ -233,16 +253,16 @@ uint64_t paced_grid(const DevCtx* c, int engine, uint64_t interleaved_width = 0)
 // compute-bound below it and run faster unpaced at full occupancy (paced at
 // 1..4 CTAs per SM: Barrett 3.9-5.6 TB/s, Montgomery 3.3-4.5,
 // tune_engines_cps.jsonl; unpaced: 6.1 / 4.8, ab_f64.jsonl).
-bool paced(int fmt, int engine) {
-    return g_pace_gbs.load() > 0.0 && (g_pace_formats.load() >> fmt & 1) &&
-           (engine == kEngFP64 || engine == kEngMixed);
+bool paced(DevCtx* c, int fmt, int engine) {
+    return (g_pace_formats.load() >> fmt & 1) && (engine == kEngFP64 || engine == kEngMixed) &&
+           pace_gbs(c) > 0.0;
 }
 
 uint64_t pace_gap_q8(int grid, double gbs, int fmt, bool constant = false) {
     // One round of the grid writes grid * 8 workers * H rows * 1 KiB;
-    // 1 GB/s == 1 byte/ns.
+    // 1 GB/s == 1 byte/ns. gbs >= kMinPaceGBs keeps this far below 2^64.
     return static_cast<uint64_t>(256.0 * grid * (kPacedThreads / 32 - 1) * paced_rows_per_round(fmt, constant) *
-                                 1024.0 / gbs);
+                                 1024.0 / std::max(gbs, kMinPaceGBs));
 }
 
 int grid_for_rows(DevCtx* c, int fmt, int engine, bool interleaved, uint64_t rows) {
@@ -346,7 +366,7 @@ cudaError_t enqueue_affine(const FillJob& j, char* dptr, uint64_t slot0, uint64_
         c.e0 = exp_add(e_first, consumed);
         c.edge[0] = edge[0];
         c.edge[1] = edge[1];
-        if (paced(j.fmt, j.engine)) {
+        if (paced(j.ctx, j.fmt, j.engine)) {
             // Paced path (by default for the 8-byte formats; f32 with the
             // FP64 engine is FP64-pipe bound below the write roof).
             constexpr uint64_t kWorkers = kPacedThreads / 32 - 1;
@@ -357,7 +377,7 @@ cudaError_t enqueue_affine(const FillJob& j, char* dptr, uint64_t slot0, uint64_
             pa.rows = rows;
             pa.e0 = c.e0;
             pa.jump = mult_for_steps(static_cast<__int128>(row) * grid * kWorkers * paced_rows_per_round(j.fmt));
-            pa.gap_q8 = pace_gap_q8(grid, g_pace_gbs.load(), j.fmt);
+            pa.gap_q8 = pace_gap_q8(grid, pace_gbs(j.ctx), j.fmt);
             pa.mode = kPacedContiguous;
             pa.edge[0] = edge[0];
             pa.edge[1] = edge[1];
@@ -451,13 +471,13 @@ cudaError_t enqueue_region(const FillJob& j, char* dptr, uint64_t slot0, uint64_
         };
         uint64_t fixed_grid = fixed_for(paced_grid(j.ctx, engine), 95);
         if (!fixed_grid && width < 250) fixed_grid = fixed_for(2ull * j.ctx->sms, 80);
-        if (paced(j.fmt, engine) && fixed_grid) {
+        if (paced(j.ctx, j.fmt, engine) && fixed_grid) {
             const uint64_t S = per_cta * fixed_grid;
             PacedArgs pa{};
             pa.out = r.out;
             pa.rows = rows;
             pa.e0 = r.e0;
-            pa.gap_q8 = pace_gap_q8(static_cast<int>(fixed_grid), g_pace_gbs.load(), j.fmt);
+            pa.gap_q8 = pace_gap_q8(static_cast<int>(fixed_grid), pace_gbs(j.ctx), j.fmt);
             pa.mode = kPacedInterleavedFixed;
             pa.q0 = r.q0;
             pa.width = width;
@@ -465,7 +485,7 @@ cudaError_t enqueue_region(const FillJob& j, char* dptr, uint64_t slot0, uint64_
             pa.wpw = p.wpw;
             pa.jump = mult_for_steps(static_cast<__int128>(S / width));
             e = launch_paced(j.fmt, engine, pa, static_cast<int>(fixed_grid), j.stream);
-        } else if (paced(j.fmt, engine)) {
+        } else if (paced(j.ctx, j.fmt, engine)) {
             // Paced, grid-strided: each stream advances nwk rows = S slots per round.
             const uint64_t want = paced_grid(j.ctx, engine, width);
             const int grid = static_cast<int>(std::max<uint64_t>(1, std::min(want, (rows + kWorkers - 1) / kWorkers)));
@@ -476,7 +496,7 @@ cudaError_t enqueue_region(const FillJob& j, char* dptr, uint64_t slot0, uint64_
             pa.out = r.out;
             pa.rows = rows;
             pa.e0 = r.e0;
-            pa.gap_q8 = pace_gap_q8(grid, g_pace_gbs.load(), j.fmt);
+            pa.gap_q8 = pace_gap_q8(grid, pace_gbs(j.ctx), j.fmt);
             pa.mode = kPacedInterleaved;
             pa.q0 = r.q0;
             pa.width = width;
@@ -737,6 +757,88 @@ bcn_status fill_host(FillJob& j, char* out, bool out_pinned) {
     return BCN_OK;
 }
 
+// Automatic pacing target of one device: the paced f64 fill (FP64 engine,
+// the default 8-byte path) timed over a sweep of targets on a 2 GiB scratch
+// buffer, 100 GB/s apart from just below its unpaced rate upwards. Below the
+// write path's collapse point the kernel holds its target; above it the rate
+// falls back towards the unpaced ~6.3 TB/s (profiles/r01/write_probe8.jsonl,
+// tune_pace.jsonl). The target is the highest one held within 2%, minus 100
+// GB/s of margin (r01 boxes: held to 7.4-7.5 TB/s -> 7.3-7.4). ~30 ms, once
+// per device and process, at context initialisation. Stream-capture safe:
+// the thread switches to relaxed capture mode and uses its own stream.
+void calibrate_pace(DevCtx* c) {
+    c->pace_cal = kDefaultPaceGBs;
+    c->pace_src = BCN_PACE_DEFAULT;
+    if (env_int("BCN_PACE_CALIBRATE", 1) == 0) return;
+    cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+    if (cudaThreadExchangeStreamCaptureMode(&mode) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    struct Scope {
+        cudaStreamCaptureMode mode;
+        void* buf = nullptr;
+        cudaEvent_t ev[2] = {nullptr, nullptr};
+        ~Scope() {
+            if (buf) cudaFree(buf);
+            for (cudaEvent_t e : ev)
+                if (e) cudaEventDestroy(e);
+            cudaThreadExchangeStreamCaptureMode(&mode);
+            cudaGetLastError();
+        }
+    } sc{mode};
+    constexpr uint64_t kItems = 1ull << 28;  // 2 GiB of doubles
+    constexpr uint64_t kRow = 128;
+    if (cudaMalloc(&sc.buf, kItems * 8) != cudaSuccess || cudaEventCreate(&sc.ev[0]) != cudaSuccess ||
+        cudaEventCreate(&sc.ev[1]) != cudaSuccess)
+        return;
+    constexpr uint64_t kWorkers = kPacedThreads / 32 - 1;
+    const int grid = c->sms * g_pace_cps.load();
+    PacedArgs pa{};
+    pa.out = sc.buf;
+    pa.rows = kItems / kRow;
+    pa.e0 = 0;
+    pa.jump = mult_for_steps(static_cast<__int128>(kRow) * grid * kWorkers * paced_rows_per_round(kFmtF64));
+    pa.mode = kPacedContiguous;
+    bool ok = true;
+    auto rate = [&](double gbs) -> double {  // GB/s over 3 launches after 1 warm-up
+        pa.gap_q8 = gbs > 0.0 ? pace_gap_q8(grid, gbs, kFmtF64) : 0;
+        ok = ok && launch_paced(kFmtF64, kEngFP64, pa, grid, c->stream) == cudaSuccess;
+        ok = ok && cudaEventRecord(sc.ev[0], c->stream) == cudaSuccess;
+        for (int i = 0; i < 3; ++i) ok = ok && launch_paced(kFmtF64, kEngFP64, pa, grid, c->stream) == cudaSuccess;
+        ok = ok && cudaEventRecord(sc.ev[1], c->stream) == cudaSuccess;
+        ok = ok && cudaEventSynchronize(sc.ev[1]) == cudaSuccess;
+        float ms = 0.0f;
+        ok = ok && cudaEventElapsedTime(&ms, sc.ev[0], sc.ev[1]) == cudaSuccess && ms > 0.0f;
+        return ok ? 3.0 * kItems * 8 / ms / 1e6 : 0.0;
+    };
+    const double unpaced = rate(0.0);
+    std::vector<std::pair<double, double>> curve;
+    double held = 0.0;
+    int misses = 0;
+    for (double t = std::floor(unpaced / 100.0) * 100.0; ok && t <= 9000.0 && misses < 3; t += 100.0) {
+        const double a = rate(t);
+        curve.emplace_back(t, a);
+        if (a >= 0.98 * t) {
+            held = t;
+            misses = 0;
+        } else {
+            ++misses;
+        }
+    }
+    if (!ok || unpaced <= 0.0) return;
+    c->pace_curve = curve;
+    c->pace_cal = held > 0.0 ? std::max(kMinPaceGBs, held - 100.0) : 0.0;
+    c->pace_src = BCN_PACE_CALIBRATED;
+}
+
+double pace_gbs(DevCtx* c) {
+    const double s = g_pace_gbs.load();
+    if (s >= 0.0) return s;
+    std::call_once(c->pace_once, [c] { calibrate_pace(c); });
+    return c->pace_cal;
+}
+
 enum class PtrKind { Device, PinnedHost, PageableHost };
 
 bcn_status classify(const void* p, int* device, PtrKind* kind) {
@@ -879,11 +981,12 @@ int bcn_auto_engine(bcn_format format) { return resolve_engine(kEngAuto, format)
 uint64_t bcn_launch_count(void) { return launch_count(); }
 
 bcn_status bcn_set_write_pacing(double target_gbs, int ctas_per_sm, int format_mask) {
-    if (!(target_gbs >= 0.0) || target_gbs > 1e5 || ctas_per_sm < 1 || ctas_per_sm > 7 ||
-        format_mask < 0 || format_mask > 7)
+    if (std::isnan(target_gbs) || target_gbs > 1e5 || (target_gbs > 0.0 && target_gbs < kMinPaceGBs) ||
+        ctas_per_sm < 1 || ctas_per_sm > 7 || format_mask < 0 || format_mask > 7)
         return fail(BCN_ERR_INVALID_ARGUMENT,
-                    "set_write_pacing: target_gbs >= 0, ctas_per_sm in [1,7], format_mask in [0,7]");
-    g_pace_gbs.store(target_gbs);
+                    "set_write_pacing: target_gbs < 0 (automatic), 0 (unpaced) or in [100, 1e5]; "
+                    "ctas_per_sm in [1,7], format_mask in [0,7]");
+    g_pace_gbs.store(target_gbs < 0.0 ? -1.0 : target_gbs);
     g_pace_cps.store(ctas_per_sm);
     g_pace_formats.store(format_mask);
     return BCN_OK;
@@ -895,6 +998,34 @@ void bcn_get_write_pacing(double* target_gbs, int* ctas_per_sm, int* format_mask
     if (target_gbs) *target_gbs = g_pace_gbs.load();
     if (ctas_per_sm) *ctas_per_sm = g_pace_cps.load();
     if (format_mask) *format_mask = g_pace_formats.load();
+}
+
+bcn_status bcn_device_write_pacing(int device, double* target_gbs, int* source) {
+    if (!target_gbs || !source) return fail(BCN_ERR_INVALID_ARGUMENT, "device_write_pacing: null output");
+    DeviceGuard guard;
+    DevCtx* c = nullptr;
+    bcn_status st = get_ctx(device < 0 ? 0 : device, &c);
+    if (st) return st;
+    const double setting = g_pace_gbs.load();
+    *target_gbs = pace_gbs(c);
+    *source = *target_gbs == 0.0 ? BCN_PACE_UNPACED : setting >= 0.0 ? BCN_PACE_USER : c->pace_src;
+    return BCN_OK;
+}
+
+bcn_status bcn_pace_calibration(int device, double* targets, double* achieved, int capacity, int* count) {
+    if (!count || capacity < 0 || (capacity > 0 && (!targets || !achieved)))
+        return fail(BCN_ERR_INVALID_ARGUMENT, "pace_calibration: bad output arrays");
+    DeviceGuard guard;
+    DevCtx* c = nullptr;
+    bcn_status st = get_ctx_nocal(device < 0 ? 0 : device, &c);
+    if (st) return st;
+    std::call_once(c->pace_once, [c] { calibrate_pace(c); });
+    *count = static_cast<int>(c->pace_curve.size());
+    for (int i = 0; i < capacity && i < *count; ++i) {
+        targets[i] = c->pace_curve[static_cast<size_t>(i)].first;
+        achieved[i] = c->pace_curve[static_cast<size_t>(i)].second;
+    }
+    return BCN_OK;
 }
 
 bcn_status bcn_set_launch_config(int ctas_per_sm, int row_order) {
@@ -1061,10 +1192,11 @@ bcn_status bcn_bench_fill(uint64_t n, uint32_t workers, bcn_layout layout, uint6
     return BCN_OK;
 }
 
-bcn_status bcn_fill_multi(void* const* outs, const int* devices, int ndev, uint64_t n,
-                          bcn_format format, uint64_t seed_index, uint64_t base_offset,
-                          bcn_engine engine) {
-    if (!outs || !devices || ndev <= 0) return fail(BCN_ERR_INVALID_ARGUMENT, "fill_multi: no devices");
+bcn_status bcn_fill_multi(void* const* outs, const uint64_t* capacities, const int* devices, int ndev,
+                          uint64_t n, bcn_format format, uint64_t seed_index, uint64_t base_offset,
+                          bcn_engine engine, void* const* streams) {
+    if (!outs || !capacities || !devices || ndev <= 0)
+        return fail(BCN_ERR_INVALID_ARGUMENT, "fill_multi: no devices");
     Plan plan;
     bcn_status st = make_plan(n, static_cast<uint32_t>(ndev), 0, &plan);
     if (st) return st;
@@ -1073,16 +1205,28 @@ bcn_status bcn_fill_multi(void* const* outs, const int* devices, int ndev, uint6
     if (plan.wpw >= (1ull << 40))
         return fail(BCN_ERR_INVALID_ARGUMENT, "fill_multi: n must be below 2^40 per device");
     const int isz = format_itemsize(format);
+    // Every shard is validated before any device work (like bcn_fill's
+    // capacity check): a short or misplaced buffer is invalid_argument, never
+    // an out-of-bounds write.
     for (uint32_t g = 0; g < plan.workers; ++g) {
         if (!outs[g]) return fail(BCN_ERR_INVALID_ARGUMENT, "fill_multi: null shard buffer");
+        if (capacities[g] < plan.elements_for(g))
+            return fail(BCN_ERR_INVALID_ARGUMENT, "fill_multi: shard " + std::to_string(g) +
+                                                      " buffer smaller than its shard of make_plan(n, ndev)");
         if (reinterpret_cast<uintptr_t>(outs[g]) % isz)
             return fail(BCN_ERR_INVALID_ARGUMENT, "fill_multi: shard buffer not aligned to its item size");
+    }
+    for (uint32_t g = 0; g < plan.workers; ++g) {
         int dev = devices[g];
         PtrKind kind;
         if ((st = classify(outs[g], &dev, &kind))) return st;
         if (kind != PtrKind::Device)
             return fail(BCN_ERR_INVALID_ARGUMENT, "fill_multi: shard buffers must be device memory");
+        for (uint32_t h = 0; h < g; ++h)
+            if (devices[h] == devices[g] && streams && streams[h] != streams[g])
+                return fail(BCN_ERR_INVALID_ARGUMENT, "fill_multi: shards on one device need one stream");
     }
+    DeviceGuard guard;
     std::vector<bcn_status> res(plan.workers, BCN_OK);
     std::vector<std::string> msg(plan.workers);
     std::vector<std::thread> pool;
@@ -1090,6 +1234,11 @@ bcn_status bcn_fill_multi(void* const* outs, const int* devices, int ndev, uint6
         pool.emplace_back([&, g] {
             DevCtx* c = nullptr;
             bcn_status s = get_ctx(devices[g], &c);
+            cudaStream_t cs = nullptr;
+            // The caller's stream for this device, or (NULL) the internal
+            // stream after the device drains, so the shard writes are ordered
+            // after every earlier use of the buffer (bcn_fill's rule).
+            if (!s) s = caller_stream(c, streams ? streams[g] : nullptr, &cs);
             if (!s) {
                 FillJob j;
                 j.plan = &plan;
@@ -1099,10 +1248,10 @@ bcn_status bcn_fill_multi(void* const* outs, const int* devices, int ndev, uint6
                 j.base_offset = base_offset;
                 j.a_exp = (seed_index - kModulus - 1) % kPeriod;
                 j.ctx = c;
-                j.stream = c->stream;
+                j.stream = cs;
                 const uint64_t p0 = static_cast<uint64_t>(g) * plan.wpw;
                 cudaError_t e = enqueue_range(j, static_cast<char*>(outs[g]), p0, p0 + plan.elements_for(g));
-                if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+                if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
                 if (e != cudaSuccess) s = cuda_fail(e, "fill_multi shard");
             }
             res[g] = s;
@@ -1305,7 +1454,8 @@ bcn_status constant_writer(const char* what, void* out, uint64_t nbytes, uint64_
     cudaStream_t s;
     if ((st = caller_stream(c, stream, &s))) return st;
     cudaError_t e;
-    if (g_pace_gbs.load() > 0.0 || noise_seed) {
+    const double pace = pace_gbs(c);
+    if (pace > 0.0 || noise_seed) {
         // The Constant writer under the same metering as the paced fill.
         constexpr uint64_t kWorkers = kPacedThreads / 32 - 1;
         const uint64_t rows = nbytes / 1024;
@@ -1315,7 +1465,7 @@ bcn_status constant_writer(const char* what, void* out, uint64_t nbytes, uint64_
         pa.out = out;
         pa.rows = rows;
         pa.e0 = pattern;
-        pa.gap_q8 = g_pace_gbs.load() > 0.0 ? pace_gap_q8(grid, g_pace_gbs.load(), kFmtU64, true) : 0;
+        pa.gap_q8 = pace > 0.0 ? pace_gap_q8(grid, pace, kFmtU64, true) : 0;
         pa.mode = kPacedConstant;
         pa.q0 = noise_seed;  // != 0: per-thread pseudo-random words instead of `pattern`
         e = launch_paced(kFmtU64, -1, pa, grid, s);

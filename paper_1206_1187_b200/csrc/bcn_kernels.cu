@@ -303,6 +303,28 @@ __device__ __forceinline__ uint64_t global_ns() {
     return t;
 }
 
+// Shared-memory mbarriers of the pacer handshake (PTX mbarrier.*, sm_90+).
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
+                 "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+                 : "memory");
+}
+// Blocks until the phase with parity `parity` has completed (try_wait sleeps
+// in hardware between probes).
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "BCN_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra BCN_WAIT;\n}" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
+        "r"(parity)
+        : "memory");
+}
+
 template <int FMT, int ENG, int MODE>
 __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a) {
     using E = Eng<ENG>;
@@ -330,24 +352,32 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
             jumps[0] = a.jump;
             jumps[1] = a.jump_wrap;
         }
-        __syncthreads();
     }
+    // Pacer handshake on two mbarriers: `release` completes one phase per
+    // round when the pacer (one thread) arrives at its scheduled time;
+    // `consumed` completes when all 8 worker warps have passed that round's
+    // release, and the pacer waits for it before releasing the next round, so
+    // no worker is ever more than one phase behind (the parity wait stays
+    // unambiguous). Workers that finish their arithmetic late store late; the
+    // pacer never waits for computation, only for the previous release to be
+    // taken. Every thread reaches the one __syncthreads() below (which also
+    // publishes `jumps`) from the same instruction: synccheck-clean
+    // (profiles/r02/sanitizers.txt), unlike r01's split aligned bar.sync.
+    __shared__ uint64_t bar_release, bar_consumed;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar_release, 1);
+        mbar_init(&bar_consumed, kWorkers);
+    }
+    __syncthreads();
     if (warp == kWorkers) {
-        // Pacer: release round k no earlier than t0 + k * gap (one timer read
-        // and one CTA barrier per round; staggering the CTAs' schedules or
-        // releasing each worker separately measured no better,
-        // profiles/r01/timeline_stagger.jsonl). Pacer and workers meet at
-        // named barrier 1 from different bar.sync instructions — the
-        // warp-specialised producer/consumer pattern of CUTLASS's
-        // NamedBarrier. compute-sanitizer synccheck reports it as divergence
-        // (tools/c/barrier_probe.cu reproduces that on a 20-line kernel);
-        // the alternatives it accepts measured slower: non-aligned
-        // barrier.sync -3.5%, one shared bar.sync instruction -9%
-        // (profiles/r01/ab_barrier.jsonl). memcheck / racecheck are clean.
-        uint64_t t0 = 0;
-        if (lane == 0) t0 = global_ns();
+        // Pacer: release round k no earlier than t0 + k * gap (staggering the
+        // CTAs' schedules or releasing each worker separately measured no
+        // better, profiles/r01/timeline_stagger.jsonl).
+        if (lane != 0) return;
+        const uint64_t t0 = global_ns();
         for (uint32_t k = 0; k < rounds; ++k) {
-            if (lane == 0 && a.gap_q8) {
+            if (k > 0) mbar_wait(&bar_consumed, (k - 1) & 1);
+            if (a.gap_q8) {
                 const uint64_t target = t0 + ((static_cast<uint64_t>(k) * a.gap_q8) >> 8);
                 uint64_t now = global_ns();
                 while (now < target) {
@@ -356,8 +386,7 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
                     now = global_ns();
                 }
             }
-            __syncwarp();
-            asm volatile("bar.sync 1, %0;" ::"n"(kPacedThreads) : "memory");
+            mbar_arrive(&bar_release);
         }
         return;
     }
@@ -440,7 +469,9 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
                     col[h][v] += same ? adv_same : adv_wrap;
                 }
         }
-        asm volatile("bar.sync 1, %0;" ::"n"(kPacedThreads) : "memory");
+        mbar_wait(&bar_release, rd & 1);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar_consumed);
         if (r + H <= count) {
 #pragma unroll
             for (int h = 0; h < H; ++h) pack_store<FMT>(p + h * hstep, bits[h]);

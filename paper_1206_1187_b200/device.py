@@ -89,14 +89,30 @@ def fill_noise(buf: torch.Tensor, seed: int = 0x1206_1187, stream=None) -> None:
 
 def fill_multi(outs: list[torch.Tensor], n: int, seed_index: int = kMinSeedIndex,
                base_offset: int = 0, fmt: Format = Format.F64,
-               engine: Engine = Engine.Auto) -> None:
+               engine: Engine = Engine.Auto, streams=None) -> None:
     """Contiguous shards of make_plan(n, len(outs)) on each tensor's device; the
-    concatenation equals a single fill of n items. Synchronous."""
+    concatenation equals a single fill of n items. Each shard is ordered after
+    the work already queued on its device's current torch stream (or on
+    `streams[g]`). Synchronous."""
+    from .parallel import _FMT_DTYPES
+
     ndev = len(outs)
-    ptrs = (ctypes.c_void_p * ndev)(*[_cuda(t, "fill_multi").data_ptr() for t in outs])
+    if ndev == 0:
+        raise InvalidArgument("fill_multi: no devices")
+    for t in outs:
+        _cuda(t, "fill_multi")
+        dt = str(t.dtype).replace("torch.", "")
+        if dt not in _FMT_DTYPES[Format(fmt)]:
+            raise InvalidArgument(f"fill_multi: {Format(fmt).name} shards need dtype "
+                                  f"{_FMT_DTYPES[Format(fmt)][0]}, got {dt}")
+    ptrs = (ctypes.c_void_p * ndev)(*[t.data_ptr() for t in outs])
+    caps = (ctypes.c_uint64 * ndev)(*[t.numel() for t in outs])
     devs = (ctypes.c_int * ndev)(*[t.device.index for t in outs])
-    _lib.call("bcn_fill_multi", ptrs, devs, ndev, n, int(fmt), seed_index,
-              base_offset & 0xFFFFFFFFFFFFFFFF, int(engine))
+    if streams is None:
+        streams = [torch.cuda.current_stream(t.device) for t in outs]
+    strs = (ctypes.c_void_p * ndev)(*[int(getattr(s, "cuda_stream", s)) for s in streams])
+    _lib.call("bcn_fill_multi", ptrs, caps, devs, ndev, n, int(fmt), seed_index,
+              base_offset & 0xFFFFFFFFFFFFFFFF, int(engine), strs)
 
 
 def set_launch_config(ctas_per_sm: int = 0, row_order: int = 1) -> None:
@@ -106,14 +122,39 @@ def set_launch_config(ctas_per_sm: int = 0, row_order: int = 1) -> None:
 
 
 def set_write_pacing(target_gbs: float, ctas_per_sm: int = 1, format_mask: int = 3) -> None:
-    """Meter the contiguous fill / Constant stores to `target_gbs` per device
-    (0 = unpaced) for the formats in `format_mask` (bit = Format value);
-    see bcn_set_write_pacing."""
+    """Meter the contiguous fill / Constant stores to `target_gbs` per device:
+    < 0 automatic (each device's calibrated target, the default), 0 unpaced,
+    else a fixed target >= 100, for the formats in `format_mask` (bit = Format
+    value); see bcn_set_write_pacing."""
     _lib.call("bcn_set_write_pacing", float(target_gbs), ctas_per_sm, format_mask)
 
 
 def write_pacing() -> float:
+    """The pacing setting (< 0 automatic, 0 unpaced, else GB/s)."""
     return float(_lib.lib().bcn_write_pacing())
+
+
+PACE_SOURCES = {0: "unpaced", 1: "user", 2: "calibrated", 3: "default"}
+
+
+def device_write_pacing(device: int = 0) -> tuple[float, str]:
+    """(effective target GB/s, source) of `device`: 'calibrated' by this
+    process's sweep at context init, 'user' (set_write_pacing), 'default'
+    (BCN_PACE_CALIBRATE=0) or 'unpaced'."""
+    g, src = ctypes.c_double(), ctypes.c_int()
+    _lib.call("bcn_device_write_pacing", device, ctypes.byref(g), ctypes.byref(src))
+    return g.value, PACE_SOURCES.get(src.value, "?")
+
+
+def pacing_source(device: int = 0) -> str:
+    return device_write_pacing(device)[1]
+
+
+def pace_calibration(device: int = 0) -> list[tuple[float, float]]:
+    """(target, achieved) GB/s points of `device`'s calibration sweep."""
+    t, a, n = (ctypes.c_double * 64)(), (ctypes.c_double * 64)(), ctypes.c_int()
+    _lib.call("bcn_pace_calibration", device, t, a, 64, ctypes.byref(n))
+    return [(t[i], a[i]) for i in range(min(n.value, 64))]
 
 
 def write_pacing_config() -> tuple[float, int, int]:

@@ -44,7 +44,7 @@ def test_library_exports_every_declared_symbol(bcn):
     # and the Python binding covers all of them
     bound = {name for name, _, _ in _lib.SIGNATURES}
     assert set(declared_symbols()) <= bound
-    assert _lib.lib().bcn_abi_version() == 1
+    assert _lib.lib().bcn_abi_version() == 2
 
 
 def test_library_is_sm100a_code(bcn):
@@ -171,3 +171,29 @@ def test_oracle_is_not_linked_into_the_product(bcn):
     ldd = subprocess.run(["ldd", _lib.LIB_PATH], capture_output=True, text=True).stdout
     assert "oracle" not in ldd and "bcnref" not in ldd
     assert ctypes  # keep import
+
+
+def test_pacing_and_multi_gpu_arguments_validated_without_device(bcn):
+    """absurd pacing targets and short fill_multi shards are
+    invalid_argument before any device work (no GPU needed to see it)."""
+    import ctypes
+
+    from paper_1206_1187_b200 import _lib
+
+    h = _lib.lib()
+    old = bcn.device.write_pacing_config()
+    try:
+        for bad in (1e-12, 50.0, 99.9, float("nan"), 2e5):
+            assert h.bcn_set_write_pacing(bad, 1, 3) == 1, bad
+        for good in (0.0, 100.0, 7200.0, -1.0):
+            assert h.bcn_set_write_pacing(good, 1, 3) == 0, good
+        assert h.bcn_write_pacing() == -1.0  # automatic
+    finally:
+        h.bcn_set_write_pacing(*old)
+    out = np.empty(64, dtype=np.float64)
+    ptrs = (ctypes.c_void_p * 2)(out.ctypes.data, out.ctypes.data)
+    devs = (ctypes.c_int * 2)(0, 0)
+    caps = (ctypes.c_uint64 * 2)(50, 49)  # make_plan(100, 2): 50 + 50
+    assert h.bcn_fill_multi(ptrs, caps, devs, 2, 100, 1, O.MIN_SEED, 0, 0, None) == 1
+    assert b"smaller than its shard" in h.bcn_last_error()
+    assert h.bcn_fill_multi(ptrs, None, devs, 2, 100, 1, O.MIN_SEED, 0, 0, None) == 1

@@ -284,6 +284,29 @@ def test_paced_kernels_bit_exact(bcn, cuda, oracle, pace):
         bcn.device.set_write_pacing(*old)
 
 
+def test_pacing_is_calibrated_per_device(bcn, cuda):
+    """Automatic pacing (the default): the device context measured its own
+    target at initialisation (no hard-coded 7200); a fixed target
+    overrides it and <0 restores it; absurd targets are rejected."""
+    old = bcn.device.write_pacing_config()
+    try:
+        bcn.device.set_write_pacing(-1, 1, 3)
+        target, src = bcn.device.device_write_pacing(0)
+        curve = bcn.device.pace_calibration(0)
+        assert src == "calibrated", (target, src, curve)
+        assert 5000 <= target <= 8500, curve
+        held = [t for t, a in curve if a >= 0.98 * t]
+        assert held and target == max(held) - 100
+        bcn.device.set_write_pacing(7100, 1, 3)
+        assert bcn.device.device_write_pacing(0) == (7100.0, "user")
+        bcn.device.set_write_pacing(0, 1, 3)
+        assert bcn.device.device_write_pacing(0) == (0.0, "unpaced")
+        bcn.device.set_write_pacing(-5, 1, 3)
+        assert bcn.device.device_write_pacing(0) == (target, "calibrated")
+    finally:
+        bcn.device.set_write_pacing(*old)
+
+
 # ------------------------------------------------------------- host buffers
 def test_host_numpy_output_chunked(bcn, cuda, oracle):
     """Host (pageable) span like the reference's std::span fill: > one 64 MiB chunk."""
@@ -477,6 +500,56 @@ def test_fill_multi_concatenation(bcn, cuda, oracle):
     assert np.array_equal(bits(got), bits(oracle.fill(n, O.FMT_F64, base_offset=31, workers=2)))
 
 
+def test_fill_multi_validates_every_shard_before_any_work(bcn, cuda):
+    """a short shard, a wrong dtype or a NULL capacity array is
+    invalid_argument and nothing is written to any shard."""
+    import ctypes
+    n = 1000
+    good = torch.full((500,), -1, dtype=torch.int64, device=cuda)
+    short = torch.full((499,), -1, dtype=torch.int64, device=cuda)
+    with pytest.raises(bcn.InvalidArgument, match="smaller than its shard"):
+        bcn.device.fill_multi([good, short], n, fmt=bcn.Format.U64)
+    assert int((good != -1).sum()) == 0 and int((short != -1).sum()) == 0
+    with pytest.raises(bcn.InvalidArgument, match="dtype"):
+        bcn.device.fill_multi([torch.empty(500, dtype=torch.float32, device=cuda)] * 2, n)
+    h = bcn._lib.lib()
+    ptrs = (ctypes.c_void_p * 1)(good.data_ptr())
+    devs = (ctypes.c_int * 1)(0)
+    assert h.bcn_fill_multi(ptrs, None, devs, 1, 100, 0, A0, 0, 0, None) == 1
+
+
+def test_fill_multi_orders_after_pending_work_on_the_stream(bcn, cuda, oracle):
+    """the shard fill runs after work already queued on the torch
+    stream that uses the buffer (a slow fill of the same buffer queued first
+    must not overwrite the multi-GPU result)."""
+    n = 1 << 26
+    out = torch.empty(n, dtype=torch.float64, device=cuda)
+    s = torch.cuda.Stream(cuda)
+    with torch.cuda.stream(s):
+        torch.cuda._sleep(50_000_000)  # ~25 ms of queued work ahead of the fill
+        out.fill_(0.25)
+        bcn.device.fill_multi([out], n, base_offset=5)
+    torch.cuda.synchronize()
+    want = oracle.fill(1 << 16, O.FMT_F64, base_offset=5 + n - (1 << 16))
+    assert np.array_equal(bits(out[-(1 << 16):].cpu().numpy()), bits(want))
+
+
+def test_fill_multi_across_all_devices(bcn, cuda, oracle):
+    """One shard per visible GPU (bcn_fill_multi's host thread per device);
+    skipped below two devices."""
+    ndev = torch.cuda.device_count()
+    if ndev < 2:
+        pytest.skip("needs >= 2 GPUs")
+    n = (1 << 27) + 12345
+    eff, wpw = oracle.make_plan(n, ndev)
+    outs = [torch.empty(min(wpw, n - g * wpw), dtype=torch.float64, device=f"cuda:{g}") for g in range(eff)]
+    bcn.device.fill_multi(outs, n, base_offset=77)
+    for g, o in enumerate(outs):
+        d = bcn.device.digest(o.view(torch.int64), index_base=g * wpw)
+        want = oracle.fill(o.numel(), O.FMT_F64, base_offset=77 + g * wpw)
+        assert d == oracle.digest(bits(want), index_base=g * wpw), g
+
+
 def test_cabi_rejects_host_buffers_where_device_memory_is_required(bcn, cuda, oracle):
     """C callers (no Python guard): host pointers passed to device-only entry
     points are rejected with BCN_ERR_INVALID_ARGUMENT before any launch, and
@@ -495,10 +568,11 @@ def test_cabi_rejects_host_buffers_where_device_memory_is_required(bcn, cuda, or
     host_out = np.empty(100, dtype=np.float64)
     ptrs = (vp * 1)(host_out.ctypes.data)
     devs = (ctypes.c_int * 1)(0)
-    st = h.bcn_fill_multi(ptrs, devs, 1, 100, 1, A0, 0, 0)
+    caps = (ctypes.c_uint64 * 1)(100)
+    st = h.bcn_fill_multi(ptrs, caps, devs, 1, 100, 1, A0, 0, 0, None)
     assert st == 1 and b"device memory" in h.bcn_last_error()
     ptrs = (vp * 1)(None)
-    assert h.bcn_fill_multi(ptrs, devs, 1, 100, 1, A0, 0, 0) == 1
+    assert h.bcn_fill_multi(ptrs, caps, devs, 1, 100, 1, A0, 0, 0, None) == 1
     # still healthy: a real call on the same context is bit-exact
     got = bcn.device.seed_states(dev_a, dev_k).cpu().numpy().view(np.uint64)
     assert got.tolist() == [oracle.state_at(A0, 0)] * 4

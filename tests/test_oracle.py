@@ -243,3 +243,26 @@ def test_c5_digest_fixture_consistent(oracle):
     with open(path) as f:
         d = json.load(f)
     assert d["log2n"] == 36 and len(d["digest"]) == 3
+
+
+def test_chunk_digest_goldens_pinned(oracle, reference):
+    """tests/golden/chunk_digests.json (per-2^24-chunk digests of the first 2^33
+    variates, every format) recomputed for sampled chunks: the oracle in all
+    three formats, the unmodified reference (oracle/_ref) in u64 and f64."""
+    path = os.path.join(os.path.dirname(__file__), "golden", "chunk_digests.json")
+    with open(path) as f:
+        g = json.load(f)
+    chunk = 1 << g["chunk_log2"]
+    assert g["seed_index"] == O.MIN_SEED and g["log2n"] == 33
+    rng = np.random.default_rng(0x1206)
+    picks = sorted({0, 63, 64, 255, 511, *rng.integers(0, 512, 2).tolist()})
+    for name, fmt in (("u64", O.FMT_U64), ("f64", O.FMT_F64), ("f32", O.FMT_F32)):
+        assert len(g["formats"][name]) == 512
+        for c in picks:
+            buf = oracle.fill(chunk, fmt, base_offset=c * chunk)
+            view = buf.view(np.uint64 if buf.itemsize == 8 else np.uint32)
+            assert [str(x) for x in oracle.digest(view, index_base=c * chunk)] == g["formats"][name][c]
+            if fmt != O.FMT_F32 and c in (0, 255):
+                rbuf = reference.fill(chunk, fmt, base_offset=c * chunk)
+                assert [str(x) for x in oracle.digest(rbuf.view(np.uint64), index_base=c * chunk)] == \
+                    g["formats"][name][c]

@@ -1,11 +1,14 @@
 # Scratch driver for one gpurun call (edited per experiment).
 set -x
-F=gpurun_out/pace
+F=gpurun_out/s1
 mkdir -p $F
-for r in 1 2; do
-  for p in 7200 6800 7000 7400 6600; do
-    timeout 600 python bench.py --pace $p --no-cpu 2>>$F/err.log | python -c "
-import json,sys
-d=json.loads(sys.stdin.read()); print(json.dumps({'pace': $p, 'rep': $r, 'value': d['value'], 'gbs': d['roofline']['achieved'], 'noise': d['roofline'].get('noise_writer_gbs'), 'clk_mean': d['clocks'].get('sm_mhz_mean'), 'power': d['clocks'].get('power_w_median')}))" >> $F/pace.jsonl
-  done
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw,power.limit --format=csv > $F/smi.txt
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider --durations=15 > $F/pytest.log 2>&1
+echo "pytest rc=$?" >> $F/pytest.log
+for fmt in f64 u64; do
+  timeout 300 python tools/ab_lib.py --libs abtest/r01.so,paper_1206_1187_b200/libbcnrand_b200.so --fmt $fmt --pace 7200 --tag mbar_vs_bar >> $F/ab.jsonl 2>>$F/ab.err
+  timeout 300 python tools/ab_lib.py --libs abtest/r01.so,paper_1206_1187_b200/libbcnrand_b200.so --fmt $fmt --tag default >> $F/ab.jsonl 2>>$F/ab.err
 done
+timeout 600 python bench.py --steps 20 --warmup 5 > $F/bench.json 2> $F/bench.err
+BCN_PACE_CALIBRATE=0 timeout 900 compute-sanitizer --tool synccheck python tools/sanitize.py > $F/synccheck.txt 2>&1
+echo "synccheck rc=$?" >> $F/synccheck.txt
