@@ -87,6 +87,7 @@ bcn_status check_seed(uint64_t a) {
 struct DevCtx {
     bool init = false;
     int sms = 148;
+    double clock_ghz = 1.965;         // maximum SM clock (cudaDevAttrClockRate)
     cudaStream_t stream = nullptr;    // internal stream for stream == NULL calls
     cudaStream_t copy[2] = {nullptr, nullptr};
     void* scratch[2] = {nullptr, nullptr};  // device chunks for host outputs
@@ -127,6 +128,9 @@ bcn_status get_ctx_nocal(int device, DevCtx** out) {
     if (!c) c = new DevCtx();
     if (!c->init) {
         BCN_CUDA(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device));
+        int khz = 0;
+        if (cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, device) == cudaSuccess && khz > 0)
+            c->clock_ghz = khz * 1e-6;
         BCN_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         BCN_CUDA(cudaStreamCreateWithFlags(&c->copy[0], cudaStreamNonBlocking));
         BCN_CUDA(cudaStreamCreateWithFlags(&c->copy[1], cudaStreamNonBlocking));
@@ -258,11 +262,24 @@ bool paced(DevCtx* c, int fmt, int engine) {
            pace_gbs(c) > 0.0;
 }
 
-uint64_t pace_gap_q8(int grid, double gbs, int fmt, bool constant = false) {
+// Pacer variant (kPaceConsumed / kPaceSmClock, bcn_kernels.cuh); exploration
+// knob BCN_PACE_FLAGS, default measured best.
+uint32_t pace_flags() {
+    static const uint32_t f = [] {
+        const char* v = std::getenv("BCN_PACE_FLAGS");
+        return v ? static_cast<uint32_t>(std::strtoul(v, nullptr, 10)) & 3u : 0u;
+    }();
+    return f;
+}
+
+uint64_t pace_gap_q8(const DevCtx* c, int grid, double gbs, int fmt, bool constant = false) {
     // One round of the grid writes grid * 8 workers * H rows * 1 KiB;
-    // 1 GB/s == 1 byte/ns. gbs >= kMinPaceGBs keeps this far below 2^64.
-    return static_cast<uint64_t>(256.0 * grid * (kPacedThreads / 32 - 1) * paced_rows_per_round(fmt, constant) *
-                                 1024.0 / std::max(gbs, kMinPaceGBs));
+    // 1 GB/s == 1 byte/ns. In SM-cycle mode the target holds at the maximum
+    // clock: bytes per cycle = gbs / clock_ghz. gbs >= kMinPaceGBs keeps this
+    // far below 2^64.
+    const double unit = (pace_flags() & kPaceSmClock) ? c->clock_ghz : 1.0;
+    return static_cast<uint64_t>(256.0 * unit * grid * (kPacedThreads / 32 - 1) *
+                                 paced_rows_per_round(fmt, constant) * 1024.0 / std::max(gbs, kMinPaceGBs));
 }
 
 int grid_for_rows(DevCtx* c, int fmt, int engine, bool interleaved, uint64_t rows) {
@@ -377,8 +394,9 @@ cudaError_t enqueue_affine(const FillJob& j, char* dptr, uint64_t slot0, uint64_
             pa.rows = rows;
             pa.e0 = c.e0;
             pa.jump = mult_for_steps(static_cast<__int128>(row) * grid * kWorkers * paced_rows_per_round(j.fmt));
-            pa.gap_q8 = pace_gap_q8(grid, pace_gbs(j.ctx), j.fmt);
+            pa.gap_q8 = pace_gap_q8(j.ctx, grid, pace_gbs(j.ctx), j.fmt);
             pa.mode = kPacedContiguous;
+            pa.pace_flags = pace_flags();
             pa.edge[0] = edge[0];
             pa.edge[1] = edge[1];
             return launch_paced(j.fmt, j.engine, pa, grid, j.stream);
@@ -477,8 +495,9 @@ cudaError_t enqueue_region(const FillJob& j, char* dptr, uint64_t slot0, uint64_
             pa.out = r.out;
             pa.rows = rows;
             pa.e0 = r.e0;
-            pa.gap_q8 = pace_gap_q8(static_cast<int>(fixed_grid), pace_gbs(j.ctx), j.fmt);
+            pa.gap_q8 = pace_gap_q8(j.ctx, static_cast<int>(fixed_grid), pace_gbs(j.ctx), j.fmt);
             pa.mode = kPacedInterleavedFixed;
+            pa.pace_flags = pace_flags();
             pa.q0 = r.q0;
             pa.width = width;
             pa.i_base = i_base;
@@ -496,8 +515,9 @@ cudaError_t enqueue_region(const FillJob& j, char* dptr, uint64_t slot0, uint64_
             pa.out = r.out;
             pa.rows = rows;
             pa.e0 = r.e0;
-            pa.gap_q8 = pace_gap_q8(grid, pace_gbs(j.ctx), j.fmt);
+            pa.gap_q8 = pace_gap_q8(j.ctx, grid, pace_gbs(j.ctx), j.fmt);
             pa.mode = kPacedInterleaved;
+            pa.pace_flags = pace_flags();
             pa.q0 = r.q0;
             pa.width = width;
             pa.i_base = i_base;
@@ -800,9 +820,10 @@ void calibrate_pace(DevCtx* c) {
     pa.e0 = 0;
     pa.jump = mult_for_steps(static_cast<__int128>(kRow) * grid * kWorkers * paced_rows_per_round(kFmtF64));
     pa.mode = kPacedContiguous;
+            pa.pace_flags = pace_flags();
     bool ok = true;
     auto rate = [&](double gbs) -> double {  // GB/s over 3 launches after 1 warm-up
-        pa.gap_q8 = gbs > 0.0 ? pace_gap_q8(grid, gbs, kFmtF64) : 0;
+        pa.gap_q8 = gbs > 0.0 ? pace_gap_q8(c, grid, gbs, kFmtF64) : 0;
         ok = ok && launch_paced(kFmtF64, kEngFP64, pa, grid, c->stream) == cudaSuccess;
         ok = ok && cudaEventRecord(sc.ev[0], c->stream) == cudaSuccess;
         for (int i = 0; i < 3; ++i) ok = ok && launch_paced(kFmtF64, kEngFP64, pa, grid, c->stream) == cudaSuccess;
@@ -1465,8 +1486,9 @@ bcn_status constant_writer(const char* what, void* out, uint64_t nbytes, uint64_
         pa.out = out;
         pa.rows = rows;
         pa.e0 = pattern;
-        pa.gap_q8 = pace > 0.0 ? pace_gap_q8(grid, pace, kFmtU64, true) : 0;
+        pa.gap_q8 = pace > 0.0 ? pace_gap_q8(c, grid, pace, kFmtU64, true) : 0;
         pa.mode = kPacedConstant;
+        pa.pace_flags = pace_flags();
         pa.q0 = noise_seed;  // != 0: per-thread pseudo-random words instead of `pattern`
         e = launch_paced(kFmtU64, -1, pa, grid, s);
     } else {

@@ -32,6 +32,7 @@
 #include <algorithm>
 #include <atomic>
 #include <mutex>
+#include <type_traits>
 
 #include "bcn_kernels.cuh"
 
@@ -162,6 +163,46 @@ __device__ __forceinline__ uint64_t emit_bits(typename E::State s) {
     }
 }
 
+// f32 from a balanced FP64 state with ONE FP64 op: the
+// canonical add (s < 0: z = s + m) is folded into the scaling FMA as
+//     y = RN(s kInv + [s < 0]),
+// which differs from x = z kInv by |1 - m kInv| <= 2^-53 when s < 0 (z >= m/4,
+// so y >= 1/4 and that is <= 2.5 ulp(y)) and equals u = RN(z kInv) exactly
+// when s > 0. RZ to 24 bits of y and of u therefore agree unless y lies within
+// 4 ulps of a 24-bit boundary (the low 29 significand bits within 4 of 0 mod
+// 2^29), probability ~2^-27 per variate; `bad` flags that case and the caller
+// recomputes the exact way (canonical add + RN multiply).
+__device__ __forceinline__ uint32_t f32_from_balanced(double s, bool& bad) {
+    const int hi = __double2hiint(s);
+    const int neg = hi >> 31;  // all ones iff s < 0
+    const double y = __fma_rn(s, kInvModulus, __hiloint2double(neg & 0x3FF00000, 0));
+    const uint32_t lo = static_cast<uint32_t>(__double2loint(y));
+    bad = neg && ((lo + 4u) & 0x1FFFFFFFu) < 8u;
+    return __float_as_uint(f32_rz_from_unit(y));
+}
+
+// The emitted bits of N streams. f32 with the FP64 engine takes the one-op
+// conversion above with a single (rarely taken) exact fallback per vector.
+template <int FMT, class E, int N>
+__device__ __forceinline__ void emit_vec(const typename E::State (&st)[N], uint64_t (&bits)[N]) {
+    if constexpr (FMT == kFmtF32 && std::is_same_v<typename E::State, double>) {
+        bool any = false;
+#pragma unroll
+        for (int v = 0; v < N; ++v) {
+            bool bad;
+            bits[v] = f32_from_balanced(st[v], bad);
+            any |= bad;
+        }
+        if (__builtin_expect(any, 0)) {
+#pragma unroll
+            for (int v = 0; v < N; ++v) bits[v] = emit_bits<FMT, E>(st[v]);
+        }
+    } else {
+#pragma unroll
+        for (int v = 0; v < N; ++v) bits[v] = emit_bits<FMT, E>(st[v]);
+    }
+}
+
 // 32-byte store: st.global.v4.b64 / v8.b32 -> SASS STG.E.256 on sm_100a.
 __device__ __forceinline__ void st256(void* p, const uint64_t (&v)[4]) {
     asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(v[0]), "l"(v[1]),
@@ -277,8 +318,7 @@ __global__ void __launch_bounds__(kContigThreads) k_fill_contig(const ContigArgs
 #pragma unroll 2
     for (; r < r_end; r += step) {
         uint64_t bits[V];
-#pragma unroll
-        for (int v = 0; v < V; ++v) bits[v] = emit_bits<FMT, E>(st[v]);
+        emit_vec<FMT, E>(st, bits);
         pack_store<FMT>(p, bits);
 #pragma unroll
         for (int v = 0; v < V; ++v) st[v] = E::mul(st[v], k);
@@ -353,20 +393,21 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
             jumps[1] = a.jump_wrap;
         }
     }
-    // Pacer handshake on two mbarriers: `release` completes one phase per
-    // round when the pacer (one thread) arrives at its scheduled time;
-    // `consumed` completes when all 8 worker warps have passed that round's
-    // release, and the pacer waits for it before releasing the next round, so
-    // no worker is ever more than one phase behind (the parity wait stays
-    // unambiguous). Workers that finish their arithmetic late store late; the
-    // pacer never waits for computation, only for the previous release to be
-    // taken. Every thread reaches the one __syncthreads() below (which also
-    // publishes `jumps`) from the same instruction: synccheck-clean
+    // Pacer handshake on shared-memory mbarriers. `release` completes one
+    // phase per round when the pacer (one thread) arrives at the round's
+    // scheduled time. Before that the pacer waits for `ready` (every worker
+    // warp has computed round k: the 8 warps then store together) or, with
+    // kPaceConsumed, for `consumed` (every worker has passed round k-1's
+    // release: workers store as soon as they are ready). Either way no worker
+    // is ever more than one phase behind, so the parity waits are unambiguous.
+    // Every thread reaches the one __syncthreads() below (which also publishes
+    // `jumps`) from the same instruction: synccheck-clean
     // (profiles/r02/sanitizers.txt), unlike r01's split aligned bar.sync.
-    __shared__ uint64_t bar_release, bar_consumed;
+    const bool consumed_proto = a.pace_flags & kPaceConsumed;
+    __shared__ uint64_t bar_release, bar_ready;
     if (threadIdx.x == 0) {
         mbar_init(&bar_release, 1);
-        mbar_init(&bar_consumed, kWorkers);
+        mbar_init(&bar_ready, kWorkers);
     }
     __syncthreads();
     if (warp == kWorkers) {
@@ -374,16 +415,20 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
         // CTAs' schedules or releasing each worker separately measured no
         // better, profiles/r01/timeline_stagger.jsonl).
         if (lane != 0) return;
-        const uint64_t t0 = global_ns();
+        const bool cycles = a.pace_flags & kPaceSmClock;
+        const uint64_t t0 = cycles ? clock64() : global_ns();
         for (uint32_t k = 0; k < rounds; ++k) {
-            if (k > 0) mbar_wait(&bar_consumed, (k - 1) & 1);
+            if (!consumed_proto)
+                mbar_wait(&bar_ready, k & 1);
+            else if (k > 0)
+                mbar_wait(&bar_ready, (k - 1) & 1);
             if (a.gap_q8) {
                 const uint64_t target = t0 + ((static_cast<uint64_t>(k) * a.gap_q8) >> 8);
-                uint64_t now = global_ns();
+                uint64_t now = cycles ? clock64() : global_ns();
                 while (now < target) {
-                    const uint64_t d = target - now;
+                    const uint64_t d = (target - now) >> (cycles ? 1 : 0);  // ~ns to wait
                     __nanosleep(d > 2048 ? 1024u : static_cast<unsigned>(d >> 1));
-                    now = global_ns();
+                    now = cycles ? clock64() : global_ns();
                 }
             }
             mbar_arrive(&bar_release);
@@ -448,14 +493,14 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
     for (uint32_t rd = 0; rd < rounds; ++rd, r += H) {
         uint64_t bits[H][V];
 #pragma unroll
-        for (int h = 0; h < H; ++h)
+        for (int h = 0; h < H; ++h) {
+            if constexpr (CONST) {
 #pragma unroll
-            for (int v = 0; v < V; ++v) {
-                if constexpr (CONST)
-                    bits[h][v] = pat[h][v];
-                else
-                    bits[h][v] = emit_bits<FMT, E>(st[h][v]);
+                for (int v = 0; v < V; ++v) bits[h][v] = pat[h][v];
+            } else {
+                emit_vec<FMT, E>(st[h], bits[h]);
             }
+        }
         // Interleaved: this round's multiplier of every stream, loaded before
         // the pacer barrier so the shared-memory latency overlaps the wait.
         Mult sel[INTER ? H : 1][INTER ? V : 1];
@@ -469,9 +514,15 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
                     col[h][v] += same ? adv_same : adv_wrap;
                 }
         }
+        if (!consumed_proto) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar_ready);
+        }
         mbar_wait(&bar_release, rd & 1);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&bar_consumed);
+        if (consumed_proto) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar_ready);
+        }
         if (r + H <= count) {
 #pragma unroll
             for (int h = 0; h < H; ++h) pack_store<FMT>(p + h * hstep, bits[h]);
@@ -524,8 +575,7 @@ __global__ void __launch_bounds__(kContigThreads) k_fill_interleaved(const Inter
     constexpr uint64_t kRowBytes = ROW * sizeof(typename Fmt<FMT>::Item);
     for (; r < r_end; ++r) {
         uint64_t bits[V];
-#pragma unroll
-        for (int v = 0; v < V; ++v) bits[v] = emit_bits<FMT, E>(st[v]);
+        emit_vec<FMT, E>(st, bits);
         pack_store<FMT>(p, bits);
 #pragma unroll
         for (int v = 0; v < V; ++v) {
