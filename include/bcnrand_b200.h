@@ -195,8 +195,8 @@ bcn_status bcn_set_launch_config(int ctas_per_sm, int row_order);
  * kernels meter their stores to a target rate (GB/s, per device) with one pacer
  * thread per CTA reading %globaltimer. target_gbs < 0: automatic (default) —
  * each device uses the target its context measured at initialisation (a short
- * sweep of the paced fill: the highest target it still holds within 2%, minus
- * 100 GB/s; BCN_PACE_CALIBRATE=0 skips the sweep and uses 7200); 0: unpaced;
+ * sweep of the paced fill, 100 GB/s apart: the target with the highest
+ * measured rate; BCN_PACE_CALIBRATE=0 skips the sweep and uses 7200); 0: unpaced;
  * otherwise a fixed target >= 100. ctas_per_sm in [1,7] (default 1: 8 worker
  * warps per SM — measured ~1.3% faster sustained than 2); format_mask: bit f
  * enables pacing for bcn_format f (default U64|F64 = 3). Output bits never

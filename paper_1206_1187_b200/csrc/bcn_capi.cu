@@ -87,7 +87,6 @@ bcn_status check_seed(uint64_t a) {
 struct DevCtx {
     bool init = false;
     int sms = 148;
-    double clock_ghz = 1.965;         // maximum SM clock (cudaDevAttrClockRate)
     cudaStream_t stream = nullptr;    // internal stream for stream == NULL calls
     cudaStream_t copy[2] = {nullptr, nullptr};
     void* scratch[2] = {nullptr, nullptr};  // device chunks for host outputs
@@ -128,9 +127,6 @@ bcn_status get_ctx_nocal(int device, DevCtx** out) {
     if (!c) c = new DevCtx();
     if (!c->init) {
         BCN_CUDA(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device));
-        int khz = 0;
-        if (cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, device) == cudaSuccess && khz > 0)
-            c->clock_ghz = khz * 1e-6;
         BCN_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         BCN_CUDA(cudaStreamCreateWithFlags(&c->copy[0], cudaStreamNonBlocking));
         BCN_CUDA(cudaStreamCreateWithFlags(&c->copy[1], cudaStreamNonBlocking));
@@ -262,24 +258,11 @@ bool paced(DevCtx* c, int fmt, int engine) {
            pace_gbs(c) > 0.0;
 }
 
-// Pacer variant (kPaceConsumed / kPaceSmClock, bcn_kernels.cuh); exploration
-// knob BCN_PACE_FLAGS, default measured best.
-uint32_t pace_flags() {
-    static const uint32_t f = [] {
-        const char* v = std::getenv("BCN_PACE_FLAGS");
-        return v ? static_cast<uint32_t>(std::strtoul(v, nullptr, 10)) & 3u : 0u;
-    }();
-    return f;
-}
-
-uint64_t pace_gap_q8(const DevCtx* c, int grid, double gbs, int fmt, bool constant = false) {
+uint64_t pace_gap_q8(int grid, double gbs, int fmt, bool constant = false) {
     // One round of the grid writes grid * 8 workers * H rows * 1 KiB;
-    // 1 GB/s == 1 byte/ns. In SM-cycle mode the target holds at the maximum
-    // clock: bytes per cycle = gbs / clock_ghz. gbs >= kMinPaceGBs keeps this
-    // far below 2^64.
-    const double unit = (pace_flags() & kPaceSmClock) ? c->clock_ghz : 1.0;
-    return static_cast<uint64_t>(256.0 * unit * grid * (kPacedThreads / 32 - 1) *
-                                 paced_rows_per_round(fmt, constant) * 1024.0 / std::max(gbs, kMinPaceGBs));
+    // 1 GB/s == 1 byte/ns. gbs >= kMinPaceGBs keeps this far below 2^64.
+    return static_cast<uint64_t>(256.0 * grid * (kPacedThreads / 32 - 1) * paced_rows_per_round(fmt, constant) *
+                                 1024.0 / std::max(gbs, kMinPaceGBs));
 }
 
 int grid_for_rows(DevCtx* c, int fmt, int engine, bool interleaved, uint64_t rows) {
@@ -394,9 +377,8 @@ cudaError_t enqueue_affine(const FillJob& j, char* dptr, uint64_t slot0, uint64_
             pa.rows = rows;
             pa.e0 = c.e0;
             pa.jump = mult_for_steps(static_cast<__int128>(row) * grid * kWorkers * paced_rows_per_round(j.fmt));
-            pa.gap_q8 = pace_gap_q8(j.ctx, grid, pace_gbs(j.ctx), j.fmt);
+            pa.gap_q8 = pace_gap_q8(grid, pace_gbs(j.ctx), j.fmt);
             pa.mode = kPacedContiguous;
-            pa.pace_flags = pace_flags();
             pa.edge[0] = edge[0];
             pa.edge[1] = edge[1];
             return launch_paced(j.fmt, j.engine, pa, grid, j.stream);
@@ -495,9 +477,8 @@ cudaError_t enqueue_region(const FillJob& j, char* dptr, uint64_t slot0, uint64_
             pa.out = r.out;
             pa.rows = rows;
             pa.e0 = r.e0;
-            pa.gap_q8 = pace_gap_q8(j.ctx, static_cast<int>(fixed_grid), pace_gbs(j.ctx), j.fmt);
+            pa.gap_q8 = pace_gap_q8(static_cast<int>(fixed_grid), pace_gbs(j.ctx), j.fmt);
             pa.mode = kPacedInterleavedFixed;
-            pa.pace_flags = pace_flags();
             pa.q0 = r.q0;
             pa.width = width;
             pa.i_base = i_base;
@@ -515,9 +496,8 @@ cudaError_t enqueue_region(const FillJob& j, char* dptr, uint64_t slot0, uint64_
             pa.out = r.out;
             pa.rows = rows;
             pa.e0 = r.e0;
-            pa.gap_q8 = pace_gap_q8(j.ctx, grid, pace_gbs(j.ctx), j.fmt);
+            pa.gap_q8 = pace_gap_q8(grid, pace_gbs(j.ctx), j.fmt);
             pa.mode = kPacedInterleaved;
-            pa.pace_flags = pace_flags();
             pa.q0 = r.q0;
             pa.width = width;
             pa.i_base = i_base;
@@ -780,12 +760,13 @@ bcn_status fill_host(FillJob& j, char* out, bool out_pinned) {
 // Automatic pacing target of one device: the paced f64 fill (FP64 engine,
 // the default 8-byte path) timed over a sweep of targets on a 2 GiB scratch
 // buffer, 100 GB/s apart from just below its unpaced rate upwards. Below the
-// write path's collapse point the kernel holds its target; above it the rate
-// falls back towards the unpaced ~6.3 TB/s (profiles/r01/write_probe8.jsonl,
-// tune_pace.jsonl). The target is the highest one held within 2%, minus 100
-// GB/s of margin (r01 boxes: held to 7.4-7.5 TB/s -> 7.3-7.4). ~30 ms, once
-// per device and process, at context initialisation. Stream-capture safe:
-// the thread switches to relaxed capture mode and uses its own stream.
+// write path's knee the kernel holds its target; above it the rate falls back
+// towards the unpaced ~6.2 TB/s (profiles/r01/write_probe8.jsonl,
+// r02/pace_modes.jsonl: 7.07 / 7.22 / 6.90 TB/s at 7200 / 7400 / 7600). The
+// target is the sweep's best point; the sweep stops 3 points after the rate
+// last rose. ~30 ms, once per device and process, at context initialisation.
+// Stream-capture safe: the thread switches to relaxed capture mode and uses
+// its own stream.
 void calibrate_pace(DevCtx* c) {
     c->pace_cal = kDefaultPaceGBs;
     c->pace_src = BCN_PACE_DEFAULT;
@@ -820,10 +801,9 @@ void calibrate_pace(DevCtx* c) {
     pa.e0 = 0;
     pa.jump = mult_for_steps(static_cast<__int128>(kRow) * grid * kWorkers * paced_rows_per_round(kFmtF64));
     pa.mode = kPacedContiguous;
-            pa.pace_flags = pace_flags();
     bool ok = true;
     auto rate = [&](double gbs) -> double {  // GB/s over 3 launches after 1 warm-up
-        pa.gap_q8 = gbs > 0.0 ? pace_gap_q8(c, grid, gbs, kFmtF64) : 0;
+        pa.gap_q8 = gbs > 0.0 ? pace_gap_q8(grid, gbs, kFmtF64) : 0;
         ok = ok && launch_paced(kFmtF64, kEngFP64, pa, grid, c->stream) == cudaSuccess;
         ok = ok && cudaEventRecord(sc.ev[0], c->stream) == cudaSuccess;
         for (int i = 0; i < 3; ++i) ok = ok && launch_paced(kFmtF64, kEngFP64, pa, grid, c->stream) == cudaSuccess;
@@ -835,21 +815,22 @@ void calibrate_pace(DevCtx* c) {
     };
     const double unpaced = rate(0.0);
     std::vector<std::pair<double, double>> curve;
-    double held = 0.0;
-    int misses = 0;
-    for (double t = std::floor(unpaced / 100.0) * 100.0; ok && t <= 9000.0 && misses < 3; t += 100.0) {
+    double best_t = 0.0, best_a = unpaced;
+    int since_best = 0;
+    for (double t = std::floor(unpaced / 100.0) * 100.0; ok && t <= 9000.0 && since_best < 3; t += 100.0) {
         const double a = rate(t);
         curve.emplace_back(t, a);
-        if (a >= 0.98 * t) {
-            held = t;
-            misses = 0;
+        if (a > best_a) {
+            best_a = a;
+            best_t = t;
+            since_best = 0;
         } else {
-            ++misses;
+            ++since_best;
         }
     }
     if (!ok || unpaced <= 0.0) return;
     c->pace_curve = curve;
-    c->pace_cal = held > 0.0 ? std::max(kMinPaceGBs, held - 100.0) : 0.0;
+    c->pace_cal = best_t;  // 0: pacing never beat the unpaced kernel
     c->pace_src = BCN_PACE_CALIBRATED;
 }
 
@@ -1335,6 +1316,7 @@ bcn_status bcn_deinterleave(const void* in, void* out, uint64_t n, uint32_t work
     t.itemsize = itemsize;
     t.order = 0;  // chosen per region by the launcher
     t.pitch = 0;
+    t.in_items = n;
     // Region 1: rows [0, sc) of all workers; region 2: the remaining
     // wpw - sc elements of workers 0..W-2 (parallel.cpp:24-33). One
     // persistent-grid launch per region.
@@ -1486,9 +1468,8 @@ bcn_status constant_writer(const char* what, void* out, uint64_t nbytes, uint64_
         pa.out = out;
         pa.rows = rows;
         pa.e0 = pattern;
-        pa.gap_q8 = pace > 0.0 ? pace_gap_q8(c, grid, pace, kFmtU64, true) : 0;
+        pa.gap_q8 = pace > 0.0 ? pace_gap_q8(grid, pace, kFmtU64, true) : 0;
         pa.mode = kPacedConstant;
-        pa.pace_flags = pace_flags();
         pa.q0 = noise_seed;  // != 0: per-thread pseudo-random words instead of `pattern`
         e = launch_paced(kFmtU64, -1, pa, grid, s);
     } else {

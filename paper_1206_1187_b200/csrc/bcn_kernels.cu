@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <algorithm>
 #include <atomic>
 #include <mutex>
@@ -185,7 +186,12 @@ __device__ __forceinline__ uint32_t f32_from_balanced(double s, bool& bad) {
 // conversion above with a single (rarely taken) exact fallback per vector.
 template <int FMT, class E, int N>
 __device__ __forceinline__ void emit_vec(const typename E::State (&st)[N], uint64_t (&bits)[N]) {
-    if constexpr (FMT == kFmtF32 && std::is_same_v<typename E::State, double>) {
+#ifndef BCN_F32_EXACT_CONVERSION
+    constexpr bool kFast = FMT == kFmtF32 && std::is_same_v<typename E::State, double>;
+#else
+    constexpr bool kFast = false;  // A/B builds: the two-op canonical conversion
+#endif
+    if constexpr (kFast) {
         bool any = false;
 #pragma unroll
         for (int v = 0; v < N; ++v) {
@@ -393,21 +399,25 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
             jumps[1] = a.jump_wrap;
         }
     }
-    // Pacer handshake on shared-memory mbarriers. `release` completes one
+    // Pacer handshake on two shared-memory mbarriers. `release` completes one
     // phase per round when the pacer (one thread) arrives at the round's
-    // scheduled time. Before that the pacer waits for `ready` (every worker
-    // warp has computed round k: the 8 warps then store together) or, with
-    // kPaceConsumed, for `consumed` (every worker has passed round k-1's
-    // release: workers store as soon as they are ready). Either way no worker
-    // is ever more than one phase behind, so the parity waits are unambiguous.
-    // Every thread reaches the one __syncthreads() below (which also publishes
-    // `jumps`) from the same instruction: synccheck-clean
-    // (profiles/r02/sanitizers.txt), unlike r01's split aligned bar.sync.
-    const bool consumed_proto = a.pace_flags & kPaceConsumed;
-    __shared__ uint64_t bar_release, bar_ready;
+    // scheduled time; `consumed` completes when all 8 worker warps have passed
+    // that round's release, and the pacer waits for it before releasing the
+    // next round, so no worker is ever more than one phase behind (the parity
+    // waits stay unambiguous). Workers compute their next rows while the pacer
+    // waits and store as soon as the release and their data are ready. (A
+    // "ready" handshake — release only once every worker has computed the
+    // round, r01's bar.sync semantics — serialises compute, two mbarrier
+    // wake-ups and the stores: 4.8 TB/s whatever the target; metering in SM
+    // cycles instead of %globaltimer ns did not raise the power-capped rate:
+    // profiles/r02/pace_modes.jsonl.) Every thread reaches the one
+    // __syncthreads() below (which also publishes `jumps`) from the same
+    // instruction: synccheck-clean (profiles/r02/sanitizers.txt), unlike r01's
+    // split aligned bar.sync.
+    __shared__ uint64_t bar_release, bar_consumed;
     if (threadIdx.x == 0) {
         mbar_init(&bar_release, 1);
-        mbar_init(&bar_ready, kWorkers);
+        mbar_init(&bar_consumed, kWorkers);
     }
     __syncthreads();
     if (warp == kWorkers) {
@@ -415,20 +425,16 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
         // CTAs' schedules or releasing each worker separately measured no
         // better, profiles/r01/timeline_stagger.jsonl).
         if (lane != 0) return;
-        const bool cycles = a.pace_flags & kPaceSmClock;
-        const uint64_t t0 = cycles ? clock64() : global_ns();
+        const uint64_t t0 = global_ns();
         for (uint32_t k = 0; k < rounds; ++k) {
-            if (!consumed_proto)
-                mbar_wait(&bar_ready, k & 1);
-            else if (k > 0)
-                mbar_wait(&bar_ready, (k - 1) & 1);
+            if (k > 0) mbar_wait(&bar_consumed, (k - 1) & 1);
             if (a.gap_q8) {
                 const uint64_t target = t0 + ((static_cast<uint64_t>(k) * a.gap_q8) >> 8);
-                uint64_t now = cycles ? clock64() : global_ns();
+                uint64_t now = global_ns();
                 while (now < target) {
-                    const uint64_t d = (target - now) >> (cycles ? 1 : 0);  // ~ns to wait
+                    const uint64_t d = target - now;
                     __nanosleep(d > 2048 ? 1024u : static_cast<unsigned>(d >> 1));
-                    now = cycles ? clock64() : global_ns();
+                    now = global_ns();
                 }
             }
             mbar_arrive(&bar_release);
@@ -514,15 +520,9 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
                     col[h][v] += same ? adv_same : adv_wrap;
                 }
         }
-        if (!consumed_proto) {
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&bar_ready);
-        }
         mbar_wait(&bar_release, rd & 1);
-        if (consumed_proto) {
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&bar_ready);
-        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar_consumed);
         if (r + H <= count) {
 #pragma unroll
             for (int h = 0; h < H; ++h) pack_store<FMT>(p + h * hstep, bits[h]);
@@ -1021,6 +1021,121 @@ __global__ void __launch_bounds__(256) k_transpose(const TransposeArgs a) {
     }
 }
 
+// Wide regions as a TMA tile mover (k_deint_bulk): a producer thread streams
+// each tile's R row segments of C = 1 KiB into shared memory with bulk async
+// copies (cp.async.bulk, SASS UBLKCP; completion counted on an mbarrier),
+// S stages deep, while 8 consumer warps drain earlier stages: a warp reads an
+// 8-row x 4-worker block (lane = row + 8 worker) and stores 4 runs of 8
+// consecutive logical items. No register prefetch (r01's k_transpose held 64
+// loads per thread in 208 registers: 1 CTA/SM); the bytes in flight live in
+// shared memory. A row segment at an arbitrary item offset is copied as the
+// 16-byte aligned window around it and read at its byte shift; the host keeps
+// windows inside the input buffer (launch_transpose). Row pitch P = 1 KiB +
+// 32 B (u64: 264 words = 8 mod 32) or + 16 B (u32: 260 = 4 mod 32) makes the
+// 8 x 4 block reads 2-way (u64, 256 B: the minimum) or <= 2-way (u32).
+template <typename T>
+struct BulkTile {
+    static constexpr int kCols = 1024 / static_cast<int>(sizeof(T));
+    static constexpr int kPitch = sizeof(T) == 8 ? 1056 : 1040;  // bytes
+};
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
+                 "r"(bytes)
+                 : "memory");
+}
+
+template <typename T, int R, int S>
+__global__ void __launch_bounds__(288) k_deint_bulk(const TransposeArgs a) {
+    using G = BulkTile<T>;
+    constexpr int C = G::kCols, P = G::kPitch;
+    constexpr int kConsumers = 8;
+    extern __shared__ __align__(128) unsigned char bulk_smem[];
+    __shared__ uint64_t full[S], empty[S];
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t ntw = (a.width + C - 1) / C;
+    const uint64_t nrb = (a.rows + R - 1) / R;
+    const uint64_t ntiles = ntw * nrb;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], kConsumers);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const char* in = static_cast<const char*>(a.in);
+    auto origin = [&](uint64_t t, uint64_t& w0, uint64_t& i0) {
+        if (a.order) {
+            w0 = (t / nrb) * C;
+            i0 = (t % nrb) * R;
+        } else {
+            w0 = (t % ntw) * C;
+            i0 = (t / ntw) * R;
+        }
+    };
+    if (warp == kConsumers) {
+        // Producer.
+        if (lane != 0) return;
+        uint32_t k = 0;
+        for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+            const uint32_t st = k % S;
+            if (k >= S) mbar_wait(&empty[st], ((k / S) - 1) & 1);
+            uint64_t w0, i0;
+            origin(t, w0, i0);
+            const uint32_t cw = static_cast<uint32_t>(a.width - w0 < C ? a.width - w0 : C);
+            const uint32_t nr = static_cast<uint32_t>(a.rows - i0 < R ? a.rows - i0 : R);
+            const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(bulk_smem)) + st * (R * P);
+            uint32_t bytes = 0;
+            for (uint32_t r = 0; r < nr; ++r) {
+                const uintptr_t lo = reinterpret_cast<uintptr_t>(in + (a.p0 + (i0 + r) * a.width + w0) * sizeof(T));
+                const uintptr_t hi = lo + cw * sizeof(T);
+                bytes += static_cast<uint32_t>(((hi + 15) & ~uintptr_t(15)) - (lo & ~uintptr_t(15)));
+            }
+            mbar_expect_tx(&full[st], bytes);
+            for (uint32_t r = 0; r < nr; ++r) {
+                const uintptr_t lo = reinterpret_cast<uintptr_t>(in + (a.p0 + (i0 + r) * a.width + w0) * sizeof(T));
+                const uintptr_t hi = lo + cw * sizeof(T);
+                const uintptr_t wlo = lo & ~uintptr_t(15);
+                bulk_g2s(base + r * P, reinterpret_cast<const void*>(wlo),
+                         static_cast<uint32_t>(((hi + 15) & ~uintptr_t(15)) - wlo), &full[st]);
+            }
+        }
+        return;
+    }
+    T* out = static_cast<T*>(a.out);
+    const unsigned rl = lane & 7, cl = lane >> 3;  // row / worker within the 8 x 4 block
+    uint32_t k = 0;
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+        const uint32_t st = k % S;
+        uint64_t w0, i0;
+        origin(t, w0, i0);
+        const uint32_t cw = static_cast<uint32_t>(a.width - w0 < C ? a.width - w0 : C);
+        const uint32_t nr = static_cast<uint32_t>(a.rows - i0 < R ? a.rows - i0 : R);
+        mbar_wait(&full[st], (k / S) & 1);
+        const unsigned char* tile = bulk_smem + st * (R * P);
+        T* dst = out + w0 * a.wpw + a.i_base + i0;
+        constexpr int kRowBlocks = R / 8, kColBlocks = C / 4;
+        for (int blk = warp; blk < kRowBlocks * kColBlocks; blk += kConsumers) {
+            const uint32_t r = (blk % kRowBlocks) * 8 + rl;
+            const uint32_t c = (blk / kRowBlocks) * 4 + cl;
+            if (r < nr && c < cw) {
+                const uintptr_t lo = reinterpret_cast<uintptr_t>(in + (a.p0 + (i0 + r) * a.width + w0) * sizeof(T));
+                const T v = *reinterpret_cast<const T*>(tile + r * P + (lo & 15) + c * sizeof(T));
+                dst[c * a.wpw + r] = v;
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+    }
+}
+
 // Narrow regions (width <= kNarrowMaxWidth workers for 4-byte items, <= 85
 // for 8-byte items; transpose_t): tiles of R whole rows
 // (R*width <= kNarrowItems slots, R a multiple of 64, or of 16 when W > 64) are one contiguous span
@@ -1382,6 +1497,51 @@ unsigned narrow_pitch_u32(unsigned W, unsigned R) {
     return best;
 }
 
+// Bulk tile mover for one wide region (k_deint_bulk). Rows whose aligned copy
+// window would end past the input buffer (only the very last row of the
+// buffer, when it does not end on 16 bytes) go to the register kernel, so no
+// copy reads outside the buffer. `variant`: 1 = R 32 / S 4 (default), 2 = R 16
+// / S 4, 3 = R 64 / S 2 (exploration knob BCN_DEINT_BULK).
+template <typename T, int R, int S>
+cudaError_t bulk_launch(const TransposeArgs& a, int sms, cudaStream_t s) {
+    const int smem = R * BulkTile<T>::kPitch * S;
+    cudaFuncSetAttribute(k_deint_bulk<T, R, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const uint64_t ntw = (a.width + BulkTile<T>::kCols - 1) / BulkTile<T>::kCols;
+    const uint64_t nrb = (a.rows + R - 1) / R;
+    const uint64_t cap = static_cast<uint64_t>(sms) * occupancy(k_deint_bulk<T, R, S>, 288, smem);
+    const uint64_t grid = std::min(ntw * nrb, cap);
+    TransposeArgs b = a;
+    // Worker blocks fastest: concurrent tiles share rows (TLB reach when a row
+    // is megabytes long), unless a worker block has many row blocks to walk.
+    b.order = (ntw < grid && nrb > 4 * grid) ? 1u : 0u;
+    k_deint_bulk<T, R, S><<<static_cast<unsigned>(grid), 288, smem, s>>>(b);
+    return counted(cudaGetLastError());
+}
+
+template <typename T>
+cudaError_t transpose_bulk(const TransposeArgs& a, int sms, int variant, cudaStream_t s) {
+    TransposeArgs head = a;
+    const uintptr_t buf_end = reinterpret_cast<uintptr_t>(a.in) + a.in_items * sizeof(T);
+    const uintptr_t last_end =
+        reinterpret_cast<uintptr_t>(a.in) + (a.p0 + a.rows * a.width) * sizeof(T);  // end of the region
+    if (((last_end + 15) & ~uintptr_t(15)) > buf_end) head.rows -= 1;
+    cudaError_t e = cudaSuccess;
+    if (head.rows) {
+        switch (variant) {
+            case 2: e = bulk_launch<T, 16, 4>(head, sms, s); break;
+            case 3: e = bulk_launch<T, 64, 2>(head, sms, s); break;
+            default: e = bulk_launch<T, 32, 4>(head, sms, s); break;
+        }
+        if (e != cudaSuccess) return e;
+    }
+    if (head.rows == a.rows) return cudaSuccess;
+    TransposeArgs tail = a;
+    tail.p0 = a.p0 + head.rows * a.width;
+    tail.rows = 1;
+    tail.i_base = a.i_base + head.rows;
+    return transpose_wide<T, 128, sizeof(T) == 8 ? 1024 : 512>(tail, sms, s);
+}
+
 template <typename T>
 cudaError_t transpose_t(const TransposeArgs& a, cudaStream_t s) {
     int dev = 0, sms = 148;
@@ -1413,6 +1573,11 @@ cudaError_t transpose_t(const TransposeArgs& a, cudaStream_t s) {
         // empty (u32 W = 129: 0.54 ms with 128-worker tiles). 256-row u32
         // tiles (1 KiB output runs) measured no better
         // (profiles/r01/deinterleave_u32_256row_negative.jsonl).
+        static const int bulk = [] {
+            const char* v = std::getenv("BCN_DEINT_BULK");
+            return v ? static_cast<int>(std::strtol(v, nullptr, 10)) : 1;
+        }();
+        if (bulk) return transpose_bulk<T>(a, sms, bulk, s);
         const uint64_t cover128 = (a.width + 127) / 128 * 128, cover64 = (a.width + 63) / 64 * 64;
         const bool wide_cols = cover128 * 10 <= cover64 * 11;
         if constexpr (sizeof(T) == 8) {

@@ -49,24 +49,14 @@ struct ContigArgs {
 // kPacedInterleavedFixed: an interleaved region whose per-round slot advance
 // is a multiple of the width, so every stream stays in its worker column and
 // steps by ONE multiplier (the contiguous kernel's stepping, interleaved seeding).
-// Pacer variants (PacedArgs.pace_flags):
-//   kPaceConsumed  release round k once every worker has passed round k-1's
-//                  release (workers store as soon as they are ready); default:
-//                  release once every worker has COMPUTED round k (all 8 warps
-//                  store together, the r01 named-barrier semantics).
-//   kPaceSmClock   meter in SM cycles (%clock64) instead of %globaltimer ns: the
-//                  write path's ceiling scales with the SM clock under the
-//                  board power cap, so a per-cycle budget follows it.
-constexpr uint32_t kPaceConsumed = 1, kPaceSmClock = 2;
 enum PacedMode : int { kPacedContiguous = 0, kPacedConstant = 1, kPacedInterleaved = 2, kPacedInterleavedFixed = 3 };
 struct PacedArgs {
     void* out;        // 32-byte aligned
     uint64_t rows;    // rows of 32 lanes x 32 bytes
     uint64_t e0;      // exponent of element 0 (or the 8-byte pattern, Constant)
     Mult jump;        // per round: contiguous 2^(53 * H * nwk * ROW); interleaved: same-row advance
-    uint64_t gap_q8;  // time between CTA rounds, x256 (0 = unpaced): ns, or SM cycles (kPaceSmClock)
+    uint64_t gap_q8;  // ns between CTA rounds, x256 (0 = unpaced)
     int mode;         // PacedMode (interleaved uses the fields below, as InterleavedArgs)
-    uint32_t pace_flags;  // kPaceConsumed | kPaceSmClock
     uint64_t q0, width, i_base, wpw, adv_b;
     Mult jump_wrap;
     EdgeRow edge[2];  // contiguous mode: partial head / tail rows (or none)
@@ -148,6 +138,7 @@ struct TransposeArgs {
     uint32_t itemsize;
     uint32_t order;   // wide tiles: 0 = worker blocks vary fastest, 1 = row blocks
     uint32_t pitch;   // narrow tiles: smem row pitch in items (0 = rows | 1)
+    uint64_t in_items;  // items of the input buffer from `in` (bulk-copy bounds)
 };
 
 // Launchers (bcn_kernels.cu). Each returns the launch error, if any.
