@@ -325,7 +325,11 @@ def main() -> None:
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     coll_dev = dev if backend == "nccl" else None
-    if world > 1:
+    # Under torchrun the process group is initialised even for one rank, so a
+    # 1-GPU run exercises the same NCCL calls (digest all-gather, timing max)
+    # as the 8-GPU one.
+    distributed = world > 1 or "TORCHELASTIC_RUN_ID" in os.environ
+    if distributed:
         if backend == "nccl":
             # Communicator init lines on stderr (rank count, transports): the
             # only NCCL traffic is the 24-byte digest all-gather and the timing max.
@@ -336,7 +340,7 @@ def main() -> None:
             dist.init_process_group(backend)
 
     def barrier():
-        if world > 1:
+        if distributed:
             dist.barrier()
 
     if args.pace is not None:
@@ -400,7 +404,7 @@ def main() -> None:
 
     def gather(vals: list[float]) -> list[list[float]]:
         """Every rank's `vals` (rank order)."""
-        if world == 1:
+        if not distributed:
             return [vals]
         t = torch.tensor(vals, dtype=torch.float64, device=coll_dev)
         out = [torch.empty_like(t) for _ in range(world)]
@@ -467,7 +471,7 @@ def main() -> None:
                               engine=engine, stream=stream)
             parts.append(B.device.digest(out_raw[:c], index_base=b))
         local_d = sharding.combine(parts)
-        glob = sharding.allgather_digest(local_d, coll_dev) if world > 1 else local_d
+        glob = sharding.allgather_digest(local_d, coll_dev) if distributed else local_d
         return glob, (None if want is None else list(glob) == list(want))
 
     want = golden_digest(args.fmt, 0, total_items) if args.workload == "c2" else \
@@ -625,7 +629,7 @@ def main() -> None:
                         f.write(json.dumps(r) + "\n")
                 line[name] = path
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if distributed:
         dist.destroy_process_group()
 
 

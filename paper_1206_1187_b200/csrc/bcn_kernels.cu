@@ -33,7 +33,6 @@
 #include <algorithm>
 #include <atomic>
 #include <mutex>
-#include <type_traits>
 
 #include "bcn_kernels.cuh"
 
@@ -164,49 +163,15 @@ __device__ __forceinline__ uint64_t emit_bits(typename E::State s) {
     }
 }
 
-// f32 from a balanced FP64 state with ONE FP64 op: the
-// canonical add (s < 0: z = s + m) is folded into the scaling FMA as
-//     y = RN(s kInv + [s < 0]),
-// which differs from x = z kInv by |1 - m kInv| <= 2^-53 when s < 0 (z >= m/4,
-// so y >= 1/4 and that is <= 2.5 ulp(y)) and equals u = RN(z kInv) exactly
-// when s > 0. RZ to 24 bits of y and of u therefore agree unless y lies within
-// 4 ulps of a 24-bit boundary (the low 29 significand bits within 4 of 0 mod
-// 2^29), probability ~2^-27 per variate; `bad` flags that case and the caller
-// recomputes the exact way (canonical add + RN multiply).
-__device__ __forceinline__ uint32_t f32_from_balanced(double s, bool& bad) {
-    const int hi = __double2hiint(s);
-    const int neg = hi >> 31;  // all ones iff s < 0
-    const double y = __fma_rn(s, kInvModulus, __hiloint2double(neg & 0x3FF00000, 0));
-    const uint32_t lo = static_cast<uint32_t>(__double2loint(y));
-    bad = neg && ((lo + 4u) & 0x1FFFFFFFu) < 8u;
-    return __float_as_uint(f32_rz_from_unit(y));
-}
-
-// The emitted bits of N streams. f32 with the FP64 engine takes the one-op
-// conversion above with a single (rarely taken) exact fallback per vector.
+// The emitted bits of N streams. (An f32 conversion with one FP64 op instead
+// of two — the canonical add folded into the scaling FMA, y = RN(s kInv +
+// [s < 0]), exact except within 4 ulps of a 24-bit boundary, with a rare exact
+// fallback — saved a DP op per variate but added ~3 integer ops and a branch:
+// 5.09 vs 5.65 TB/s median, 5.78 vs 6.35 best, profiles/r02/ab_f32_conversion.jsonl.)
 template <int FMT, class E, int N>
 __device__ __forceinline__ void emit_vec(const typename E::State (&st)[N], uint64_t (&bits)[N]) {
-#ifndef BCN_F32_EXACT_CONVERSION
-    constexpr bool kFast = FMT == kFmtF32 && std::is_same_v<typename E::State, double>;
-#else
-    constexpr bool kFast = false;  // A/B builds: the two-op canonical conversion
-#endif
-    if constexpr (kFast) {
-        bool any = false;
 #pragma unroll
-        for (int v = 0; v < N; ++v) {
-            bool bad;
-            bits[v] = f32_from_balanced(st[v], bad);
-            any |= bad;
-        }
-        if (__builtin_expect(any, 0)) {
-#pragma unroll
-            for (int v = 0; v < N; ++v) bits[v] = emit_bits<FMT, E>(st[v]);
-        }
-    } else {
-#pragma unroll
-        for (int v = 0; v < N; ++v) bits[v] = emit_bits<FMT, E>(st[v]);
-    }
+    for (int v = 0; v < N; ++v) bits[v] = emit_bits<FMT, E>(st[v]);
 }
 
 // 32-byte store: st.global.v4.b64 / v8.b32 -> SASS STG.E.256 on sm_100a.
@@ -1056,8 +1021,10 @@ __global__ void __launch_bounds__(288) k_deint_bulk(const TransposeArgs a) {
     using G = BulkTile<T>;
     constexpr int C = G::kCols, P = G::kPitch;
     constexpr int kConsumers = 8;
+    static_assert(R % 8 == 0 && R <= 64, "rows per tile");
     extern __shared__ __align__(128) unsigned char bulk_smem[];
     __shared__ uint64_t full[S], empty[S];
+    __shared__ uint8_t shift[S][R];  // byte offset of each row segment in its window
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t ntw = (a.width + C - 1) / C;
     const uint64_t nrb = (a.rows + R - 1) / R;
@@ -1070,7 +1037,7 @@ __global__ void __launch_bounds__(288) k_deint_bulk(const TransposeArgs a) {
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    const char* in = static_cast<const char*>(a.in);
+    const uintptr_t in = reinterpret_cast<uintptr_t>(a.in);
     auto origin = [&](uint64_t t, uint64_t& w0, uint64_t& i0) {
         if (a.order) {
             w0 = (t / nrb) * C;
@@ -1081,8 +1048,9 @@ __global__ void __launch_bounds__(288) k_deint_bulk(const TransposeArgs a) {
         }
     };
     if (warp == kConsumers) {
-        // Producer.
-        if (lane != 0) return;
+        // Producer warp: lane l computes the copy windows of rows l, l + 32;
+        // lane 0 arms the stage's barrier with their total, then every lane
+        // issues its own bulk copies.
         uint32_t k = 0;
         for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
             const uint32_t st = k % S;
@@ -1091,21 +1059,30 @@ __global__ void __launch_bounds__(288) k_deint_bulk(const TransposeArgs a) {
             origin(t, w0, i0);
             const uint32_t cw = static_cast<uint32_t>(a.width - w0 < C ? a.width - w0 : C);
             const uint32_t nr = static_cast<uint32_t>(a.rows - i0 < R ? a.rows - i0 : R);
-            const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(bulk_smem)) + st * (R * P);
+            constexpr int kPer = (R + 31) / 32;  // rows per producer lane
+            uintptr_t wlo[kPer];
+            uint32_t wsz[kPer];
             uint32_t bytes = 0;
-            for (uint32_t r = 0; r < nr; ++r) {
-                const uintptr_t lo = reinterpret_cast<uintptr_t>(in + (a.p0 + (i0 + r) * a.width + w0) * sizeof(T));
-                const uintptr_t hi = lo + cw * sizeof(T);
-                bytes += static_cast<uint32_t>(((hi + 15) & ~uintptr_t(15)) - (lo & ~uintptr_t(15)));
+#pragma unroll
+            for (int j = 0; j < kPer; ++j) {
+                const uint32_t r = lane + 32 * j;
+                wsz[j] = 0;
+                if (r < nr) {
+                    const uintptr_t lo = in + (a.p0 + (i0 + r) * a.width + w0) * sizeof(T);
+                    const uintptr_t hi = lo + cw * sizeof(T);
+                    wlo[j] = lo & ~uintptr_t(15);
+                    wsz[j] = static_cast<uint32_t>(((hi + 15) & ~uintptr_t(15)) - wlo[j]);
+                    shift[st][r] = static_cast<uint8_t>(lo & 15);
+                    bytes += wsz[j];
+                }
             }
-            mbar_expect_tx(&full[st], bytes);
-            for (uint32_t r = 0; r < nr; ++r) {
-                const uintptr_t lo = reinterpret_cast<uintptr_t>(in + (a.p0 + (i0 + r) * a.width + w0) * sizeof(T));
-                const uintptr_t hi = lo + cw * sizeof(T);
-                const uintptr_t wlo = lo & ~uintptr_t(15);
-                bulk_g2s(base + r * P, reinterpret_cast<const void*>(wlo),
-                         static_cast<uint32_t>(((hi + 15) & ~uintptr_t(15)) - wlo), &full[st]);
-            }
+            bytes = __reduce_add_sync(0xffffffffu, bytes);
+            if (lane == 0) mbar_expect_tx(&full[st], bytes);
+            __syncwarp();
+            const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(bulk_smem)) + st * (R * P);
+#pragma unroll
+            for (int j = 0; j < kPer; ++j)
+                if (wsz[j]) bulk_g2s(base + (lane + 32 * j) * P, reinterpret_cast<const void*>(wlo[j]), wsz[j], &full[st]);
         }
         return;
     }
@@ -1122,14 +1099,13 @@ __global__ void __launch_bounds__(288) k_deint_bulk(const TransposeArgs a) {
         const unsigned char* tile = bulk_smem + st * (R * P);
         T* dst = out + w0 * a.wpw + a.i_base + i0;
         constexpr int kRowBlocks = R / 8, kColBlocks = C / 4;
+#pragma unroll 4
         for (int blk = warp; blk < kRowBlocks * kColBlocks; blk += kConsumers) {
             const uint32_t r = (blk % kRowBlocks) * 8 + rl;
             const uint32_t c = (blk / kRowBlocks) * 4 + cl;
-            if (r < nr && c < cw) {
-                const uintptr_t lo = reinterpret_cast<uintptr_t>(in + (a.p0 + (i0 + r) * a.width + w0) * sizeof(T));
-                const T v = *reinterpret_cast<const T*>(tile + r * P + (lo & 15) + c * sizeof(T));
-                dst[c * a.wpw + r] = v;
-            }
+            if (r < nr && c < cw)
+                dst[static_cast<uint64_t>(c) * a.wpw + r] =
+                    *reinterpret_cast<const T*>(tile + r * P + shift[st][r] + c * sizeof(T));
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);

@@ -139,6 +139,10 @@ def fill_format(out, plan: PartitionPlan, seed_index: int, method: Method, base_
                 fmt: Format, *, engine: Engine = Engine.Auto, stream=None,
                 sync: bool = False) -> None:
     """Common body of fill / fill_residues / fill_float (parallel.cpp:56-79)."""
+    from .generator import OutOfRange, check_u64
+
+    check_u64(plan.n, "fill")
+    check_u64(seed_index, "seed_from_index", OutOfRange)
     ptr, cap, dt, is_cuda, dev, tensor = _buffer(out)
     if dt not in _FMT_DTYPES[Format(fmt)]:
         raise InvalidArgument(f"fill: {Format(fmt).name} output needs dtype {_FMT_DTYPES[Format(fmt)][0]}, got {dt}")

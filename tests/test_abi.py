@@ -197,3 +197,27 @@ def test_pacing_and_multi_gpu_arguments_validated_without_device(bcn):
     assert h.bcn_fill_multi(ptrs, caps, devs, 2, 100, 1, O.MIN_SEED, 0, 0, None) == 1
     assert b"smaller than its shard" in h.bcn_last_error()
     assert h.bcn_fill_multi(ptrs, None, devs, 2, 100, 1, O.MIN_SEED, 0, 0, None) == 1
+
+
+def test_python_mirror_matches_reference_scalar_semantics(bcn):
+    """next() on z = 0 returns 0 for every method but
+    BarrettModified (generator.hpp:52-70 with modred.hpp:150), and Python ints
+    outside [0, 2^64) are rejected instead of truncated by ctypes."""
+    g = bcn.gen
+    for m in (g.Method.Ref128, g.Method.LEcuyer, g.Method.Barrett):
+        s = g.GeneratorState(O.MIN_SEED, 0, 5, m)
+        assert g.next(s) == 0 and s.k == 6
+    with pytest.raises(bcn.DomainError):
+        g.next(g.GeneratorState(O.MIN_SEED, 0, 0, g.Method.BarrettModified))
+    with pytest.raises(bcn.OutOfRange):
+        g.seed_from_index((1 << 64) + O.MIN_SEED)  # would truncate to a valid seed
+    with pytest.raises(bcn.OutOfRange):
+        g.state_at(-1, 0)
+    with pytest.raises(bcn.DomainError):
+        g.to_unit_interval((1 << 64) + 5)
+    with pytest.raises(bcn.InvalidArgument):
+        g.modpow2(1 << 64, 7)
+    assert g.state_at(O.MIN_SEED, -1).z == g.state_at(O.MIN_SEED, (1 << 64) - 1).z  # k wraps like u64
+    buf = np.empty(8, dtype=np.float64)
+    with pytest.raises(bcn.OutOfRange):
+        bcn.par.fill(buf, bcn.par.make_plan(8, 1), (1 << 64) + O.MIN_SEED)

@@ -723,3 +723,28 @@ def test_bench_two_ranks_share_one_gpu(bcn, cuda):
     buf = torch.empty(n, dtype=torch.float64, device=cuda)
     bcn.par.fill(buf, bcn.par.make_plan(n, 1), O.MIN_SEED, sync=True)
     assert [str(x) for x in bcn.device.digest(buf.view(torch.int64))] == line["digest"]
+
+
+def test_bench_nccl_branch_world_one(bcn, cuda):
+    """bench.py under torchrun with the NCCL backend at world size 1 (the
+    driver's 8-GPU launch, one rank): the process group, the digest
+    all-gather and the max-over-ranks timing run through NCCL, the NCCL INIT
+    lines reach stderr, and the line carries per-rank times and a verified
+    digest (C2 and the C5 strong-scaling section)."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k != "BCN_DIST_BACKEND"}
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
+           "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(root, "bench.py"),
+           "--gpus", "1", "--steps", "3", "--warmup", "3", "--no-e2e", "--no-cpu", "--sustain-s", "0",
+           "--c5-steps", "1"]
+    r = subprocess.run(cmd, capture_output=True, text=True, env=env, cwd=root, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 1 and line["digest_verified_vs_oracle"] is True
+    assert line["c5_strong"]["digest_verified_vs_oracle"] is True
+    assert [p["rank"] for p in line["per_rank"]] == [0]
+    assert "NCCL INFO" in r.stderr and "nranks 1" in r.stderr.replace("nRanks", "nranks")

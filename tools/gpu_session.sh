@@ -1,14 +1,9 @@
 # Scratch driver for one gpurun call (edited per experiment).
 set -x
-F=gpurun_out/s3
+F=gpurun_out/s4
 mkdir -p $F
 timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider -x > $F/pytest.log 2>&1; echo "pytest rc=$?" >> $F/pytest.log
-for rep in 1 2; do
-  timeout 300 python tools/ab_lib.py --libs abtest/r01.so,paper_1206_1187_b200/libbcnrand_b200.so,abtest/f32exact.so --fmt f32 --tag f32conv >> $F/ab.jsonl 2>>$F/ab.err
-  timeout 300 python tools/ab_lib.py --libs abtest/r01.so,paper_1206_1187_b200/libbcnrand_b200.so --fmt f64 --pace 7400 --tag consumed >> $F/ab.jsonl 2>>$F/ab.err
-  timeout 300 python tools/ab_lib.py --libs abtest/r01.so,paper_1206_1187_b200/libbcnrand_b200.so --fmt u64 --pace 7400 --tag consumed >> $F/ab.jsonl 2>>$F/ab.err
-done
-W=1,2,7,16,31,33,64,85,86,100,128,129,200,1000,5003,100003,1000000
+W=7,64,85,86,100,128,129,200,1000,5003,100003,1000000
 for v in 0 1 2 3; do
   BCN_DEINT_BULK=$v timeout 600 python tools/deint_perf.py $W | sed "s/^{/{\"bulk\": $v, /" >> $F/deint.jsonl 2>>$F/deint.err
 done
