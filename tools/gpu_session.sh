@@ -1,10 +1,9 @@
 # Scratch driver for one gpurun call (edited per experiment).
 set -x
-F=gpurun_out/s4
+F=gpurun_out/s5
 mkdir -p $F
-timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider -x > $F/pytest.log 2>&1; echo "pytest rc=$?" >> $F/pytest.log
-W=7,64,85,86,100,128,129,200,1000,5003,100003,1000000
-for v in 0 1 2 3; do
-  BCN_DEINT_BULK=$v timeout 600 python tools/deint_perf.py $W | sed "s/^{/{\"bulk\": $v, /" >> $F/deint.jsonl 2>>$F/deint.err
+M="--set full --clock-control none --import-source on"
+for cfg in "0 4 1000000" "1 4 1000000" "0 4 200" "1 4 200" "0 8 86" "1 8 86" "0 8 1000000" "0 4 100"; do
+  set -- $cfg
+  BCN_DEINT_BULK=$1 timeout 600 ncu $M -k regex:"transpose|deint" -s 3 -c 1 -o $F/deint_b$1_i$2_w$3 python tools/deint_one.py --isz $2 --w $3 > $F/ncu_b$1_i$2_w$3.log 2>&1
 done
-timeout 600 python bench.py --steps 20 --warmup 5 > $F/bench.json 2> $F/bench.err
