@@ -349,10 +349,16 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t nwk = static_cast<uint64_t>(gridDim.x) * kWorkers;
     const uint64_t first = static_cast<uint64_t>(blockIdx.x) * kWorkers;
-    // Worker w writes rows w + (H*k + h)*nwk, h < H; a round covers H*nwk rows.
-    const uint64_t per_round = H * nwk;
-    const uint32_t rounds =
-        a.rows > first ? static_cast<uint32_t>((a.rows - first + per_round - 1) / per_round) : 0;
+    // Worker w writes 1 KiB rows (ROW slots) at slots w*ROW + (H*k + h)*D,
+    // h < H, for D = nwk*ROW (grid-strided rows; a round covers H*nwk rows) or
+    // the interleaved super-row length a.row_stride (a multiple of the width
+    // and of the 32-byte chunk; workers whose row would start past it idle).
+    const uint64_t D = a.row_stride ? a.row_stride : nwk * ROW;
+    const uint64_t N = a.rows * ROW;  // slots
+    const uint64_t first_slot = first * ROW;
+    const uint32_t rounds = first_slot < N && first_slot < D
+                                ? static_cast<uint32_t>(((N - first_slot + D - 1) / D + H - 1) / H)
+                                : 0;
     if constexpr (!CONST && !INTER_SEED) fill_edges<FMT>(a.edge);
     if (rounds == 0) return;  // uniform across the CTA
     // Interleaved: the two jump multipliers in shared memory, so a stream picks
@@ -407,8 +413,10 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
         return;
     }
     const uint64_t w = first + warp;
-    // rows this worker owns: w, w+nwk, ... (< a.rows)
-    const uint32_t count = a.rows > w ? static_cast<uint32_t>((a.rows - w + nwk - 1) / nwk) : 0;
+    // Rows this lane's chunk takes part in (its chunk is whole or absent in
+    // every row: D and N are multiples of the 32-byte chunk).
+    const uint64_t w_slot = w * ROW + lane * V;
+    const uint32_t count = w_slot < D && w_slot < N ? static_cast<uint32_t>((N - w_slot + D - 1) / D) : 0;
     typename E::State st[H][V];
     // interleaved: worker index of each stream's slot (< width < 2^32). A
     // stream stays in the same physical row iff col < same_below; col then
@@ -436,18 +444,17 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
     if (!CONST) {
 #pragma unroll
         for (int h = 0; h < H; ++h) {
-            const uint64_t row = w + h * nwk;
             if constexpr (INTER_SEED) {
 #pragma unroll
                 for (int v = 0; v < V; ++v) {
-                    const uint64_t q = a.q0 + row * ROW + lane * V + v;
+                    const uint64_t q = a.q0 + w_slot + h * D + v;
                     const uint64_t c = q % a.width;
                     if constexpr (INTER) col[h][v] = static_cast<uint32_t>(c);
                     const uint64_t j = c * a.wpw + a.i_base + q / a.width;
                     st[h][v] = E::from_canonical(dev_state_from_exp(dev_exp_at(a.e0, j)));
                 }
             } else {
-                uint64_t z = dev_state_from_exp(dev_exp_at(a.e0, row * ROW + lane * V));
+                uint64_t z = dev_state_from_exp(dev_exp_at(a.e0, w_slot + h * D));
 #pragma unroll
                 for (int v = 0; v < V; ++v) {
                     st[h][v] = E::from_canonical(z);
@@ -456,9 +463,8 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
             }
         }
     }
-    constexpr uint64_t kRowBytes = ROW * sizeof(typename Fmt<FMT>::Item);
-    char* p = static_cast<char*>(a.out) + w * kRowBytes + lane * 32;
-    const uint64_t hstep = nwk * kRowBytes;
+    char* p = static_cast<char*>(a.out) + w_slot * sizeof(typename Fmt<FMT>::Item);
+    const uint64_t hstep = D * sizeof(typename Fmt<FMT>::Item);
     const Mult k = a.jump;
     uint32_t r = 0;  // this worker's rows done
     for (uint32_t rd = 0; rd < rounds; ++rd, r += H) {

@@ -59,6 +59,7 @@ struct PacedArgs {
     int mode;         // PacedMode (interleaved uses the fields below, as InterleavedArgs)
     uint64_t q0, width, i_base, wpw, adv_b;
     Mult jump_wrap;
+    uint64_t row_stride;  // slots between a worker's consecutive rows (0: grid * 8 rows)
     EdgeRow edge[2];  // contiguous mode: partial head / tail rows (or none)
 };
 
