@@ -258,11 +258,15 @@ bool paced(DevCtx* c, int fmt, int engine) {
            pace_gbs(c) > 0.0;
 }
 
+// Pacer period (ns x 256) for `bytes_per_round` at `gbs` (1 GB/s == 1 byte/ns;
+// gbs >= kMinPaceGBs keeps this far below 2^64).
+uint64_t pace_gap_q8_bytes(double bytes_per_round, double gbs) {
+    return static_cast<uint64_t>(256.0 * bytes_per_round / std::max(gbs, kMinPaceGBs));
+}
+
+// One round of a grid-strided paced grid writes grid * 8 workers * H rows * 1 KiB.
 uint64_t pace_gap_q8(int grid, double gbs, int fmt, bool constant = false) {
-    // One round of the grid writes grid * 8 workers * H rows * 1 KiB;
-    // 1 GB/s == 1 byte/ns. gbs >= kMinPaceGBs keeps this far below 2^64.
-    return static_cast<uint64_t>(256.0 * grid * (kPacedThreads / 32 - 1) * paced_rows_per_round(fmt, constant) *
-                                 1024.0 / std::max(gbs, kMinPaceGBs));
+    return pace_gap_q8_bytes(1024.0 * grid * (kPacedThreads / 32 - 1) * paced_rows_per_round(fmt, constant), gbs);
 }
 
 int grid_for_rows(DevCtx* c, int fmt, int engine, bool interleaved, uint64_t rows) {
@@ -450,41 +454,48 @@ cudaError_t enqueue_region(const FillJob& j, char* dptr, uint64_t slot0, uint64_
                                          static_cast<__int128>(p.wpw) +
                                      adv_a + 1);
         constexpr uint64_t kWorkers = kPacedThreads / 32 - 1;
-        // Column-stable paced grid: a round advances every stream by
-        // S = row * kWorkers * H * grid slots; when width divides S the stream
-        // stays in its worker column and steps by one multiplier (S / width
-        // elements), as in the contiguous kernel. The grid must then be a
-        // multiple of width / gcd(width, row * kWorkers * H): taken if such a
-        // grid keeps >= 95% of the contiguous grid (W = 7: 147 CTAs, W = 64:
-        // 148), or, for W < 250, >= 80% of a 2-CTA-per-SM grid (W = 125: 250
-        // CTAs); profiles/r01/interleaved_fixed*.jsonl. From W = 250 the
-        // two-multiplier mode (multiplier loads hoisted above the pacer
-        // barrier) matches or beats the uneven 250-CTA grid (W = 250 / 1000 /
-        // 2000: +2 / +4 / +0-5%; interleaved_fixed_vs_two_mult.jsonl).
-        const uint64_t per_cta = row * kWorkers * paced_rows_per_round(j.fmt);
-        const uint64_t unit = width / std::gcd(width, per_cta);
-        const uint64_t need = std::max<uint64_t>(1, (rows + kWorkers - 1) / kWorkers);
-        auto fixed_for = [&](uint64_t base, uint64_t pct) -> uint64_t {
-            base = std::min(base, need);
-            const uint64_t g = base / unit * unit;
-            return g >= 1 && g * 100 >= base * pct ? g : 0;
-        };
-        uint64_t fixed_grid = fixed_for(paced_grid(j.ctx, engine), 95);
-        if (!fixed_grid && width < 250) fixed_grid = fixed_for(2ull * j.ctx->sms, 80);
-        if (paced(j.ctx, j.fmt, engine) && fixed_grid) {
-            const uint64_t S = per_cta * fixed_grid;
+        // Column-stable super-rows: the region is cut into super-rows of L
+        // slots, L a multiple of both the width and the 32-byte chunk (lcm x
+        // k0, the largest that fits the grid's workers); worker w writes the
+        // 1 KiB block at w * row of every super-row (the last block of a
+        // super-row is partial, whole chunks; workers past it idle). A slot
+        // and the same slot one super-row later hold the same worker column,
+        // L / width elements apart, so every stream steps by ONE multiplier —
+        // the contiguous kernel's arithmetic with interleaved seeding — for
+        // any width whose lcm fits: u64 up to ~37k workers with 1 CTA per SM,
+        // ~113k with 3. Taken when >= 90% of the grid's workers have a block
+        // (profiles/r02/interleaved_super.jsonl); otherwise the
+        // two-multiplier mode below.
+        const uint64_t chunk = 32 / isz;
+        const uint64_t lcm = width / std::gcd(width, chunk) * chunk;
+        const int H = paced_rows_per_round(j.fmt);
+        uint64_t sr_grid = 0, sr_len = 0;
+        for (int cps = 1; cps <= 3 && !sr_grid; ++cps) {
+            const uint64_t nwk = static_cast<uint64_t>(j.ctx->sms) * cps * kWorkers;
+            const uint64_t k0 = row * nwk / lcm;
+            const uint64_t L = k0 * lcm;
+            if (k0 && (L + row - 1) / row * 10 >= nwk * 9) {
+                sr_grid = static_cast<uint64_t>(j.ctx->sms) * cps;
+                sr_len = L;
+            }
+        }
+        if (paced(j.ctx, j.fmt, engine) && sr_grid) {
+            const uint64_t n_slots = rows * row;
+            const uint64_t busy = (std::min(sr_len, n_slots) + row - 1) / row;  // workers with a block
+            const uint64_t grid = std::min(sr_grid, (busy + kWorkers - 1) / kWorkers);
             PacedArgs pa{};
             pa.out = r.out;
             pa.rows = rows;
             pa.e0 = r.e0;
-            pa.gap_q8 = pace_gap_q8(static_cast<int>(fixed_grid), pace_gbs(j.ctx), j.fmt);
+            pa.gap_q8 = pace_gap_q8_bytes(static_cast<double>(H) * std::min(sr_len, n_slots) * isz, pace_gbs(j.ctx));
             pa.mode = kPacedInterleavedFixed;
             pa.q0 = r.q0;
             pa.width = width;
             pa.i_base = i_base;
             pa.wpw = p.wpw;
-            pa.jump = mult_for_steps(static_cast<__int128>(S / width));
-            e = launch_paced(j.fmt, engine, pa, static_cast<int>(fixed_grid), j.stream);
+            pa.row_stride = sr_len;
+            pa.jump = mult_for_steps(static_cast<__int128>(H) * (sr_len / width));
+            e = launch_paced(j.fmt, engine, pa, static_cast<int>(grid), j.stream);
         } else if (paced(j.ctx, j.fmt, engine)) {
             // Paced, grid-strided: each stream advances nwk rows = S slots per round.
             const uint64_t want = paced_grid(j.ctx, engine, width);

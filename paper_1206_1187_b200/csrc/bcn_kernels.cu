@@ -1022,11 +1022,12 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                  : "memory");
 }
 
+constexpr int kBulkConsumers = 16;
 template <typename T, int R, int S>
-__global__ void __launch_bounds__(288) k_deint_bulk(const TransposeArgs a) {
+__global__ void __launch_bounds__(kBulkConsumers * 32 + 32) k_deint_bulk(const TransposeArgs a) {
     using G = BulkTile<T>;
     constexpr int C = G::kCols, P = G::kPitch;
-    constexpr int kConsumers = 8;
+    constexpr int kConsumers = kBulkConsumers;
     static_assert(R % 8 == 0 && R <= 64, "rows per tile");
     extern __shared__ __align__(128) unsigned char bulk_smem[];
     __shared__ uint64_t full[S], empty[S];
@@ -1105,13 +1106,24 @@ __global__ void __launch_bounds__(288) k_deint_bulk(const TransposeArgs a) {
         const unsigned char* tile = bulk_smem + st * (R * P);
         T* dst = out + w0 * a.wpw + a.i_base + i0;
         constexpr int kRowBlocks = R / 8, kColBlocks = C / 4;
-#pragma unroll 4
-        for (int blk = warp; blk < kRowBlocks * kColBlocks; blk += kConsumers) {
-            const uint32_t r = (blk % kRowBlocks) * 8 + rl;
-            const uint32_t c = (blk / kRowBlocks) * 4 + cl;
-            if (r < nr && c < cw)
-                dst[static_cast<uint64_t>(c) * a.wpw + r] =
-                    *reinterpret_cast<const T*>(tile + r * P + shift[st][r] + c * sizeof(T));
+        constexpr int kBlocks = kRowBlocks * kColBlocks, kBatch = 4;
+        static_assert(kBlocks % (kConsumers * kBatch) == 0, "blocks per warp");
+        // Batches of 4 blocks: 4 shared-memory loads in flight, then 4 stores.
+        for (int b0 = warp; b0 < kBlocks; b0 += kConsumers * kBatch) {
+            T v[kBatch];
+            uint32_t rr[kBatch], cc[kBatch];
+#pragma unroll
+            for (int u = 0; u < kBatch; ++u) {
+                const int blk = b0 + u * kConsumers;
+                rr[u] = (blk % kRowBlocks) * 8 + rl;
+                cc[u] = (blk / kRowBlocks) * 4 + cl;
+                v[u] = rr[u] < nr && cc[u] < cw
+                           ? *reinterpret_cast<const T*>(tile + rr[u] * P + shift[st][rr[u]] + cc[u] * sizeof(T))
+                           : T(0);
+            }
+#pragma unroll
+            for (int u = 0; u < kBatch; ++u)
+                if (rr[u] < nr && cc[u] < cw) dst[static_cast<uint64_t>(cc[u]) * a.wpw + rr[u]] = v[u];
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);
@@ -1490,13 +1502,13 @@ cudaError_t bulk_launch(const TransposeArgs& a, int sms, cudaStream_t s) {
     cudaFuncSetAttribute(k_deint_bulk<T, R, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const uint64_t ntw = (a.width + BulkTile<T>::kCols - 1) / BulkTile<T>::kCols;
     const uint64_t nrb = (a.rows + R - 1) / R;
-    const uint64_t cap = static_cast<uint64_t>(sms) * occupancy(k_deint_bulk<T, R, S>, 288, smem);
+    const uint64_t cap = static_cast<uint64_t>(sms) * occupancy(k_deint_bulk<T, R, S>, kBulkConsumers * 32 + 32, smem);
     const uint64_t grid = std::min(ntw * nrb, cap);
     TransposeArgs b = a;
     // Worker blocks fastest: concurrent tiles share rows (TLB reach when a row
     // is megabytes long), unless a worker block has many row blocks to walk.
     b.order = (ntw < grid && nrb > 4 * grid) ? 1u : 0u;
-    k_deint_bulk<T, R, S><<<static_cast<unsigned>(grid), 288, smem, s>>>(b);
+    k_deint_bulk<T, R, S><<<static_cast<unsigned>(grid), kBulkConsumers * 32 + 32, smem, s>>>(b);
     return counted(cudaGetLastError());
 }
 

@@ -33,6 +33,8 @@ def main() -> None:
     p.add_argument("--log2n", type=int, default=30)
     p.add_argument("--engine", type=int, default=0)
     p.add_argument("--tag", default="")
+    p.add_argument("--workers", type=int, default=1, help="plan workers (with --interleaved: the width W)")
+    p.add_argument("--interleaved", action="store_true")
     a = p.parse_args()
     fmt = {"u64": 0, "f64": 1, "f32": 2}[a.fmt]
     isz = 4 if a.fmt == "f32" else 8
@@ -55,7 +57,8 @@ def main() -> None:
     times = {path: [] for path, _ in libs}
 
     def launch(lib):
-        st = lib.bcn_fill(ctypes.c_void_p(buf.data_ptr()), n, n, fmt, 1, 0, A0, 3, 0, a.engine, 0, sp)
+        st = lib.bcn_fill(ctypes.c_void_p(buf.data_ptr()), n, n, fmt, a.workers, int(a.interleaved), A0, 3, 0,
+                          a.engine, 0, sp)
         if st:
             raise RuntimeError(lib.bcn_last_error())
 
@@ -76,6 +79,7 @@ def main() -> None:
     for path, v in times.items():
         med = statistics.median(v)
         print(json.dumps({"tag": a.tag, "lib": path, "fmt": a.fmt, "pace": a.pace, "log2n": a.log2n,
+                          "workers": a.workers, "layout": "interleaved" if a.interleaved else "contiguous",
                           "median_ms": med, "min_ms": min(v), "gbs_median": n * isz / med / 1e6,
                           "gbs_best": n * isz / min(v) / 1e6, "samples": len(v)}), flush=True)
 

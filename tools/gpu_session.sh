@@ -1,13 +1,12 @@
 # Scratch driver for one gpurun call (edited per experiment).
 set -x
-F=gpurun_out/s5
+F=gpurun_out/s6
 mkdir -p $F
-M="--set full --clock-control none --import-source on"
-for cfg in "0 4 1000000" "1 4 1000000" "0 4 200" "1 4 200" "0 8 86" "1 8 86" "0 8 1000000" "0 4 100"; do
-  set -- $cfg
-  R=/tmp/deint_b$1_i$2_w$3
-  BCN_DEINT_BULK=$1 timeout 600 ncu $M -k regex:"transpose|deint" -s 3 -c 1 -o $R python tools/deint_one.py --isz $2 --w $3 > $F/ncu_b$1_i$2_w$3.log 2>&1
-  ncu -i $R.ncu-rep --page raw --csv > $F/raw_b$1_i$2_w$3.csv 2>&1
-  ncu -i $R.ncu-rep --page details --csv > $F/details_b$1_i$2_w$3.csv 2>&1
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider -x > $F/pytest.log 2>&1; echo "pytest rc=$?" >> $F/pytest.log
+for W in 7 64 125 250 1001 5003 100003; do
+  timeout 300 python tools/ab_lib.py --libs abtest/r01.so,paper_1206_1187_b200/libbcnrand_b200.so --fmt f64 --pace 7200 --interleaved --workers $W --rounds 8 --tag inter >> $F/inter.jsonl 2>>$F/inter.err
 done
-ls -la $F
+W=7,64,86,100,128,129,200,1000,5003,100003,1000000
+for v in 0 1 2 3; do
+  BCN_DEINT_BULK=$v timeout 600 python tools/deint_perf.py $W | sed "s/^{/{\"bulk\": $v, /" >> $F/deint.jsonl 2>>$F/deint.err
+done
