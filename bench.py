@@ -333,8 +333,9 @@ def main() -> None:
         if backend == "nccl":
             # Communicator init lines on stderr (rank count, transports): the
             # only NCCL traffic is the 24-byte digest all-gather and the timing max.
-            os.environ.setdefault("NCCL_DEBUG", "INFO")
-            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            if os.environ.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
+                os.environ["NCCL_DEBUG"] = "INFO"
+                os.environ["NCCL_DEBUG_SUBSYS"] = "INIT"
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)

@@ -463,9 +463,12 @@ cudaError_t enqueue_region(const FillJob& j, char* dptr, uint64_t slot0, uint64_
         // L / width elements apart, so every stream steps by ONE multiplier —
         // the contiguous kernel's arithmetic with interleaved seeding — for
         // any width whose lcm fits: u64 up to ~37k workers with 1 CTA per SM,
-        // ~113k with 3. Taken when >= 90% of the grid's workers have a block
-        // (profiles/r02/interleaved_super.jsonl); otherwise the
-        // two-multiplier mode below.
+        // ~113k with 3. Taken with the fewest CTAs per SM (1..3) at which
+        // >= 95% of the workers have a block: W = 125 / 250 / 1001 at 1 CTA
+        // per SM, +6 / +3 / +2% over r01's modes; W = 5003 with 92.5% at 1 CTA
+        // per SM measured 3% slower than two multipliers, so it takes 2
+        // (profiles/r02/interleaved_super.jsonl). Otherwise the two-multiplier
+        // mode below.
         const uint64_t chunk = 32 / isz;
         const uint64_t lcm = width / std::gcd(width, chunk) * chunk;
         const int H = paced_rows_per_round(j.fmt);
@@ -474,7 +477,7 @@ cudaError_t enqueue_region(const FillJob& j, char* dptr, uint64_t slot0, uint64_
             const uint64_t nwk = static_cast<uint64_t>(j.ctx->sms) * cps * kWorkers;
             const uint64_t k0 = row * nwk / lcm;
             const uint64_t L = k0 * lcm;
-            if (k0 && (L + row - 1) / row * 10 >= nwk * 9) {
+            if (k0 && (L + row - 1) / row * 100 >= nwk * 95) {
                 sr_grid = static_cast<uint64_t>(j.ctx->sms) * cps;
                 sr_len = L;
             }

@@ -992,144 +992,6 @@ __global__ void __launch_bounds__(256) k_transpose(const TransposeArgs a) {
     }
 }
 
-// Wide regions as a TMA tile mover (k_deint_bulk): a producer thread streams
-// each tile's R row segments of C = 1 KiB into shared memory with bulk async
-// copies (cp.async.bulk, SASS UBLKCP; completion counted on an mbarrier),
-// S stages deep, while 8 consumer warps drain earlier stages: a warp reads an
-// 8-row x 4-worker block (lane = row + 8 worker) and stores 4 runs of 8
-// consecutive logical items. No register prefetch (r01's k_transpose held 64
-// loads per thread in 208 registers: 1 CTA/SM); the bytes in flight live in
-// shared memory. A row segment at an arbitrary item offset is copied as the
-// 16-byte aligned window around it and read at its byte shift; the host keeps
-// windows inside the input buffer (launch_transpose). Row pitch P = 1 KiB +
-// 32 B (u64: 264 words = 8 mod 32) or + 16 B (u32: 260 = 4 mod 32) makes the
-// 8 x 4 block reads 2-way (u64, 256 B: the minimum) or <= 2-way (u32).
-template <typename T>
-struct BulkTile {
-    static constexpr int kCols = 1024 / static_cast<int>(sizeof(T));
-    static constexpr int kPitch = sizeof(T) == 8 ? 1056 : 1040;  // bytes
-};
-
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-                 "l"(src), "r"(bytes), "r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                     static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
-                 "r"(bytes)
-                 : "memory");
-}
-
-constexpr int kBulkConsumers = 16;
-template <typename T, int R, int S>
-__global__ void __launch_bounds__(kBulkConsumers * 32 + 32) k_deint_bulk(const TransposeArgs a) {
-    using G = BulkTile<T>;
-    constexpr int C = G::kCols, P = G::kPitch;
-    constexpr int kConsumers = kBulkConsumers;
-    static_assert(R % 8 == 0 && R <= 64, "rows per tile");
-    extern __shared__ __align__(128) unsigned char bulk_smem[];
-    __shared__ uint64_t full[S], empty[S];
-    __shared__ uint8_t shift[S][R];  // byte offset of each row segment in its window
-    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t ntw = (a.width + C - 1) / C;
-    const uint64_t nrb = (a.rows + R - 1) / R;
-    const uint64_t ntiles = ntw * nrb;
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < S; ++i) {
-            mbar_init(&full[i], 1);
-            mbar_init(&empty[i], kConsumers);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    const uintptr_t in = reinterpret_cast<uintptr_t>(a.in);
-    auto origin = [&](uint64_t t, uint64_t& w0, uint64_t& i0) {
-        if (a.order) {
-            w0 = (t / nrb) * C;
-            i0 = (t % nrb) * R;
-        } else {
-            w0 = (t % ntw) * C;
-            i0 = (t / ntw) * R;
-        }
-    };
-    if (warp == kConsumers) {
-        // Producer warp: lane l computes the copy windows of rows l, l + 32;
-        // lane 0 arms the stage's barrier with their total, then every lane
-        // issues its own bulk copies.
-        uint32_t k = 0;
-        for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
-            const uint32_t st = k % S;
-            if (k >= S) mbar_wait(&empty[st], ((k / S) - 1) & 1);
-            uint64_t w0, i0;
-            origin(t, w0, i0);
-            const uint32_t cw = static_cast<uint32_t>(a.width - w0 < C ? a.width - w0 : C);
-            const uint32_t nr = static_cast<uint32_t>(a.rows - i0 < R ? a.rows - i0 : R);
-            constexpr int kPer = (R + 31) / 32;  // rows per producer lane
-            uintptr_t wlo[kPer];
-            uint32_t wsz[kPer];
-            uint32_t bytes = 0;
-#pragma unroll
-            for (int j = 0; j < kPer; ++j) {
-                const uint32_t r = lane + 32 * j;
-                wsz[j] = 0;
-                if (r < nr) {
-                    const uintptr_t lo = in + (a.p0 + (i0 + r) * a.width + w0) * sizeof(T);
-                    const uintptr_t hi = lo + cw * sizeof(T);
-                    wlo[j] = lo & ~uintptr_t(15);
-                    wsz[j] = static_cast<uint32_t>(((hi + 15) & ~uintptr_t(15)) - wlo[j]);
-                    shift[st][r] = static_cast<uint8_t>(lo & 15);
-                    bytes += wsz[j];
-                }
-            }
-            bytes = __reduce_add_sync(0xffffffffu, bytes);
-            if (lane == 0) mbar_expect_tx(&full[st], bytes);
-            __syncwarp();
-            const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(bulk_smem)) + st * (R * P);
-#pragma unroll
-            for (int j = 0; j < kPer; ++j)
-                if (wsz[j]) bulk_g2s(base + (lane + 32 * j) * P, reinterpret_cast<const void*>(wlo[j]), wsz[j], &full[st]);
-        }
-        return;
-    }
-    T* out = static_cast<T*>(a.out);
-    const unsigned rl = lane & 7, cl = lane >> 3;  // row / worker within the 8 x 4 block
-    uint32_t k = 0;
-    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
-        const uint32_t st = k % S;
-        uint64_t w0, i0;
-        origin(t, w0, i0);
-        const uint32_t cw = static_cast<uint32_t>(a.width - w0 < C ? a.width - w0 : C);
-        const uint32_t nr = static_cast<uint32_t>(a.rows - i0 < R ? a.rows - i0 : R);
-        mbar_wait(&full[st], (k / S) & 1);
-        const unsigned char* tile = bulk_smem + st * (R * P);
-        T* dst = out + w0 * a.wpw + a.i_base + i0;
-        constexpr int kRowBlocks = R / 8, kColBlocks = C / 4;
-        constexpr int kBlocks = kRowBlocks * kColBlocks, kBatch = 4;
-        static_assert(kBlocks % (kConsumers * kBatch) == 0, "blocks per warp");
-        // Batches of 4 blocks: 4 shared-memory loads in flight, then 4 stores.
-        for (int b0 = warp; b0 < kBlocks; b0 += kConsumers * kBatch) {
-            T v[kBatch];
-            uint32_t rr[kBatch], cc[kBatch];
-#pragma unroll
-            for (int u = 0; u < kBatch; ++u) {
-                const int blk = b0 + u * kConsumers;
-                rr[u] = (blk % kRowBlocks) * 8 + rl;
-                cc[u] = (blk / kRowBlocks) * 4 + cl;
-                v[u] = rr[u] < nr && cc[u] < cw
-                           ? *reinterpret_cast<const T*>(tile + rr[u] * P + shift[st][rr[u]] + cc[u] * sizeof(T))
-                           : T(0);
-            }
-#pragma unroll
-            for (int u = 0; u < kBatch; ++u)
-                if (rr[u] < nr && cc[u] < cw) dst[static_cast<uint64_t>(cc[u]) * a.wpw + rr[u]] = v[u];
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[st]);
-    }
-}
-
 // Narrow regions (width <= kNarrowMaxWidth workers for 4-byte items, <= 85
 // for 8-byte items; transpose_t): tiles of R whole rows
 // (R*width <= kNarrowItems slots, R a multiple of 64, or of 16 when W > 64) are one contiguous span
@@ -1491,51 +1353,6 @@ unsigned narrow_pitch_u32(unsigned W, unsigned R) {
     return best;
 }
 
-// Bulk tile mover for one wide region (k_deint_bulk). Rows whose aligned copy
-// window would end past the input buffer (only the very last row of the
-// buffer, when it does not end on 16 bytes) go to the register kernel, so no
-// copy reads outside the buffer. `variant`: 1 = R 32 / S 4 (default), 2 = R 16
-// / S 4, 3 = R 64 / S 2 (exploration knob BCN_DEINT_BULK).
-template <typename T, int R, int S>
-cudaError_t bulk_launch(const TransposeArgs& a, int sms, cudaStream_t s) {
-    const int smem = R * BulkTile<T>::kPitch * S;
-    cudaFuncSetAttribute(k_deint_bulk<T, R, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    const uint64_t ntw = (a.width + BulkTile<T>::kCols - 1) / BulkTile<T>::kCols;
-    const uint64_t nrb = (a.rows + R - 1) / R;
-    const uint64_t cap = static_cast<uint64_t>(sms) * occupancy(k_deint_bulk<T, R, S>, kBulkConsumers * 32 + 32, smem);
-    const uint64_t grid = std::min(ntw * nrb, cap);
-    TransposeArgs b = a;
-    // Worker blocks fastest: concurrent tiles share rows (TLB reach when a row
-    // is megabytes long), unless a worker block has many row blocks to walk.
-    b.order = (ntw < grid && nrb > 4 * grid) ? 1u : 0u;
-    k_deint_bulk<T, R, S><<<static_cast<unsigned>(grid), kBulkConsumers * 32 + 32, smem, s>>>(b);
-    return counted(cudaGetLastError());
-}
-
-template <typename T>
-cudaError_t transpose_bulk(const TransposeArgs& a, int sms, int variant, cudaStream_t s) {
-    TransposeArgs head = a;
-    const uintptr_t buf_end = reinterpret_cast<uintptr_t>(a.in) + a.in_items * sizeof(T);
-    const uintptr_t last_end =
-        reinterpret_cast<uintptr_t>(a.in) + (a.p0 + a.rows * a.width) * sizeof(T);  // end of the region
-    if (((last_end + 15) & ~uintptr_t(15)) > buf_end) head.rows -= 1;
-    cudaError_t e = cudaSuccess;
-    if (head.rows) {
-        switch (variant) {
-            case 2: e = bulk_launch<T, 16, 4>(head, sms, s); break;
-            case 3: e = bulk_launch<T, 64, 2>(head, sms, s); break;
-            default: e = bulk_launch<T, 32, 4>(head, sms, s); break;
-        }
-        if (e != cudaSuccess) return e;
-    }
-    if (head.rows == a.rows) return cudaSuccess;
-    TransposeArgs tail = a;
-    tail.p0 = a.p0 + head.rows * a.width;
-    tail.rows = 1;
-    tail.i_base = a.i_base + head.rows;
-    return transpose_wide<T, 128, sizeof(T) == 8 ? 1024 : 512>(tail, sms, s);
-}
-
 template <typename T>
 cudaError_t transpose_t(const TransposeArgs& a, cudaStream_t s) {
     int dev = 0, sms = 148;
@@ -1567,11 +1384,6 @@ cudaError_t transpose_t(const TransposeArgs& a, cudaStream_t s) {
         // empty (u32 W = 129: 0.54 ms with 128-worker tiles). 256-row u32
         // tiles (1 KiB output runs) measured no better
         // (profiles/r01/deinterleave_u32_256row_negative.jsonl).
-        static const int bulk = [] {
-            const char* v = std::getenv("BCN_DEINT_BULK");
-            return v ? static_cast<int>(std::strtol(v, nullptr, 10)) : 1;
-        }();
-        if (bulk) return transpose_bulk<T>(a, sms, bulk, s);
         const uint64_t cover128 = (a.width + 127) / 128 * 128, cover64 = (a.width + 63) / 64 * 64;
         const bool wide_cols = cover128 * 10 <= cover64 * 11;
         if constexpr (sizeof(T) == 8) {
