@@ -1384,6 +1384,23 @@ cudaError_t transpose_t(const TransposeArgs& a, cudaStream_t s) {
         // empty (u32 W = 129: 0.54 ms with 128-worker tiles). 256-row u32
         // tiles (1 KiB output runs) measured no better
         // (profiles/r01/deinterleave_u32_256row_negative.jsonl).
+        static const int shape = [] {  // exploration knob: force one wide tile shape
+            const char* v = std::getenv("BCN_DEINT_WIDE");
+            return v ? static_cast<int>(std::strtol(v, nullptr, 10)) : 0;
+        }();
+        switch (shape) {
+            case 1: return transpose_wide<T, 128, 1024>(a, sms, s);
+            case 2: return transpose_wide<T, 64, 1024>(a, sms, s);
+            case 3: return transpose_wide<T, 32, 1024>(a, sms, s);
+            case 4:
+                if constexpr (sizeof(T) == 8) return transpose_wide<T, 64, 2048>(a, sms, s);
+                break;
+            case 5:
+                if constexpr (sizeof(T) == 8) return transpose_wide<T, 32, 2048>(a, sms, s);
+                break;
+            case 6: return transpose_wide<T, 128, 512>(a, sms, s);
+            default: break;
+        }
         const uint64_t cover128 = (a.width + 127) / 128 * 128, cover64 = (a.width + 63) / 64 * 64;
         const bool wide_cols = cover128 * 10 <= cover64 * 11;
         if constexpr (sizeof(T) == 8) {

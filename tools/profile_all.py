@@ -4,7 +4,7 @@
 
     ncu --set full --clock-control none --import-source on -o gpurun_out/prof_all \
         python tools/profile_all.py
-    python tools/ncu_summary.py gpurun_out/prof_all.ncu-rep -o profiles/r01/ncu_full_all_kernels.json
+    python tools/ncu_summary.py gpurun_out/prof_all.ncu-rep -o profiles/r02/ncu_full_all_kernels.json
 """
 from __future__ import annotations
 
@@ -42,6 +42,10 @@ def main() -> None:
         ("staged f64 (paper T=1 + TMA)", lambda: fill(f64, B.Format.F64, B.Engine.Staged)),
         ("paced interleaved W=7 (column-stable)", lambda: fill(f64, B.Format.F64,
                                                                p=B.par.make_plan(n, 7, B.Layout.Interleaved))),
+        ("paced interleaved W=1001 (super-rows)", lambda: fill(f64, B.Format.F64,
+                                                                p=B.par.make_plan(n, 1001, B.Layout.Interleaved))),
+        ("paced interleaved W=5003 (super-rows, 2 CTAs/SM)",
+         lambda: fill(f64, B.Format.F64, p=B.par.make_plan(n, 5003, B.Layout.Interleaved))),
         ("paced interleaved W=100003 (two multipliers)",
          lambda: fill(f64, B.Format.F64, p=B.par.make_plan(n, 100003, B.Layout.Interleaved))),
         ("paced constant", lambda: B.device.fill_constant(u64)),
@@ -67,7 +71,7 @@ def main() -> None:
         sync()
         fn()
         sync()
-    B.device.set_write_pacing(7200, 1, 3)
+    B.device.set_write_pacing(-1, 1, 3)  # back to the calibrated target
     # small / auxiliary kernels
     small = torch.empty(100003 + 1, dtype=torch.float64, device=dev)[1:]
     B.par.fill(small, B.par.make_plan(100003, 3), A0, base_offset=(1 << 64) - 50000)  # slots (wrap)
