@@ -35,6 +35,8 @@ def main() -> None:
     p.add_argument("--tag", default="")
     p.add_argument("--workers", type=int, default=1, help="plan workers (with --interleaved: the width W)")
     p.add_argument("--interleaved", action="store_true")
+    p.add_argument("--cps", type=int, default=1, help="paced CTAs per SM (with --pace)")
+    p.add_argument("--mask", type=int, default=3, help="paced format mask (with --pace; 7 = f32 too)")
     a = p.parse_args()
     fmt = {"u64": 0, "f64": 1, "f32": 2}[a.fmt]
     isz = 4 if a.fmt == "f32" else 8
@@ -52,7 +54,7 @@ def main() -> None:
         lib.bcn_set_write_pacing.argtypes = [ctypes.c_double, ctypes.c_int, ctypes.c_int]
         lib.bcn_last_error.restype = ctypes.c_char_p
         if a.pace is not None:
-            assert lib.bcn_set_write_pacing(a.pace, 1, 3) == 0
+            assert lib.bcn_set_write_pacing(a.pace, a.cps, a.mask) == 0
         libs.append((path, lib))
     times = {path: [] for path, _ in libs}
 
@@ -78,7 +80,7 @@ def main() -> None:
             times[path] += [evs[i].elapsed_time(evs[i + 1]) for i in range(a.per)]
     for path, v in times.items():
         med = statistics.median(v)
-        print(json.dumps({"tag": a.tag, "lib": path, "fmt": a.fmt, "pace": a.pace, "log2n": a.log2n,
+        print(json.dumps({"tag": a.tag, "lib": path, "fmt": a.fmt, "pace": a.pace, "cps": a.cps, "mask": a.mask, "log2n": a.log2n,
                           "workers": a.workers, "layout": "interleaved" if a.interleaved else "contiguous",
                           "median_ms": med, "min_ms": min(v), "gbs_median": n * isz / med / 1e6,
                           "gbs_best": n * isz / min(v) / 1e6, "samples": len(v)}), flush=True)
