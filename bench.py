@@ -286,7 +286,17 @@ def ncu_traffic(kernel: str, algorithmic_bytes: float) -> tuple[float | None, st
     import glob
 
     best = None
-    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_full_*.json"))):
+    # Newest round first: its capture is of the code being measured.
+    for rdir in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*")), reverse=True):
+        if best is not None:
+            break
+        best = _ncu_best(kernel, algorithmic_bytes, sorted(glob.glob(os.path.join(rdir, "ncu_full_*.json"))))
+    return (best[1], best[2]) if best else (None, None)
+
+
+def _ncu_best(kernel: str, algorithmic_bytes: float, paths: list[str]):
+    best = None
+    for path in paths:
         try:
             with open(path) as f:
                 rows = json.load(f)
@@ -297,7 +307,7 @@ def ncu_traffic(kernel: str, algorithmic_bytes: float) -> tuple[float | None, st
                 d = abs(r["traffic_bytes"] - algorithmic_bytes)
                 if best is None or d < best[0]:
                     best = (d, r["traffic_bytes"], os.path.relpath(path, ROOT))
-    return (best[1], best[2]) if best else (None, None)
+    return best
 
 
 def main() -> None:

@@ -188,11 +188,7 @@ constexpr int kPacedThreads = 288;  // 8 worker warps + 1 pacer warp
 // streams per lane) and for the Constant writer (no compute spreads its
 // stores, and a 2-row burst per round measurably lowers HBM efficiency).
 __host__ __device__ constexpr int paced_rows_per_round(int fmt, bool constant = false) {
-#ifdef BCN_F32_PACED_H2  // A/B builds
-    return constant ? 1 : 2;
-#else
     return (constant || fmt == kFmtF32) ? 1 : 2;
-#endif
 }
 // Measured default pacing target for the 8-byte formats (DESIGN.md §5,
 // profiles/r01/tune_pace.jsonl): FP64 engine f64/u64 reach ~7.08 TB/s at

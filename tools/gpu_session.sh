@@ -1,10 +1,27 @@
-# Scratch driver for one gpurun call (edited per experiment).
+# Final evidence pass on the round-2 code (one gpurun call).
 set -x
-F=gpurun_out/s9
+F=gpurun_out/s10
 mkdir -p $F
-for cps in 1 2 3; do
-  for pace in 6800 7200; do
-    timeout 300 python tools/ab_lib.py --libs paper_1206_1187_b200/libbcnrand_b200.so,abtest/f32h2.so --fmt f32 --pace $pace --cps $cps --mask 7 --rounds 6 --tag f32h2 >> $F/f32h2.jsonl 2>>$F/err.log
-  done
+nvidia-smi --query-gpu=name,serial,clocks.sm,clocks.max.sm,power.draw,power.limit --format=csv > $F/smi.txt
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider --durations=30 > $F/pytest.log 2>&1; echo "pytest rc=$?" >> $F/pytest.log
+timeout 900 python bench.py --steps 20 --warmup 5 > $F/bench_default.json 2> $F/bench_default.err
+timeout 900 python bench.py --impl reference --steps 20 --warmup 5 > $F/bench_reference_arm.json 2> $F/bench_reference_arm.err
+PACE=$(python -c "import json;print(json.load(open('$F/bench_default.json'))['launch']['write_pacing_gbs'])")
+for v in "--fmt u64" "--fmt f32" "--engine barrett" "--engine montgomery" "--engine staged" "--engine bulk" "--engine mixed"; do
+  timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu --no-e2e --no-c5 $v >> $F/bench_variants.jsonl 2>> $F/bench_variants.err
 done
-timeout 300 python tools/ab_lib.py --libs paper_1206_1187_b200/libbcnrand_b200.so --fmt f32 --pace 0 --rounds 6 --tag f32unpaced >> $F/f32h2.jsonl 2>>$F/err.log
+timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e --no-c5 --sustain-s 0 --sweep $F/sweep_c3.jsonl > /dev/null 2>> $F/sweep.err
+W=1,2,7,16,31,33,64,85,86,100,128,129,200,1000,5003,100003,1000000
+timeout 600 python tools/deint_perf.py $W > $F/deinterleave_final.jsonl 2>> $F/deint.err
+for W in 7 64 125 250 1001 5003 20000 100003; do
+  timeout 300 python tools/ab_lib.py --libs paper_1206_1187_b200/libbcnrand_b200.so --fmt f64 --interleaved --workers $W --rounds 4 --tag interleaved_final >> $F/interleaved_final.jsonl 2>>$F/inter.err
+done
+BCN_PACE_CALIBRATE=0 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $F/launches_bench.csv python bench.py --steps 20 --warmup 3 --no-cpu --no-e2e --no-c5 --sustain-s 0 --pace $PACE > $F/launches_bench.log 2>&1
+BCN_PACE_CALIBRATE=0 timeout 1800 ncu --set full --clock-control none --import-source on -o /tmp/prof_all python tools/profile_all.py --pace $PACE > $F/prof_all.log 2>&1
+python tools/ncu_summary.py /tmp/prof_all.ncu-rep -o $F/ncu_full_all_kernels.json >> $F/prof_all.log 2>&1
+python tools/ncu_summary.py --launches $F/launches_bench.csv -o $F/launches_bench.json >> $F/prof_all.log 2>&1
+for tool in memcheck racecheck synccheck; do
+  BCN_PACE_CALIBRATE=0 timeout 1200 compute-sanitizer --tool $tool python tools/sanitize.py > $F/sanitize_$tool.txt 2>&1
+  echo "rc=$?" >> $F/sanitize_$tool.txt
+done
+ls -la $F

@@ -22,6 +22,11 @@ A0 = B.kMinSeedIndex
 
 
 def main() -> None:
+    # `--pace X`: profile the paced kernels at a fixed target (e.g. the one the
+    # bench's calibration chose on this box) instead of recalibrating under ncu.
+    if "--pace" in sys.argv:
+        B.device.set_write_pacing(float(sys.argv[sys.argv.index("--pace") + 1]), 1, 3)
+    pace = B.device.write_pacing_config()
     dev = torch.device("cuda:0")
     n = 1 << 30
     f64 = torch.empty(n, dtype=torch.float64, device=dev)
@@ -71,7 +76,7 @@ def main() -> None:
         sync()
         fn()
         sync()
-    B.device.set_write_pacing(-1, 1, 3)  # back to the calibrated target
+    B.device.set_write_pacing(*pace)
     # small / auxiliary kernels
     small = torch.empty(100003 + 1, dtype=torch.float64, device=dev)[1:]
     B.par.fill(small, B.par.make_plan(100003, 3), A0, base_offset=(1 << 64) - 50000)  # slots (wrap)
