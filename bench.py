@@ -2,7 +2,7 @@
 """Benchmark of the alpha_{2,3} fill path on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--fmt f64|u64|f32] [--engine auto|barrett|montgomery|fp64|staged|bulk|mixed]
+                    [--fmt f64|u64|f32] [--engine auto|barrett|montgomery|fp64|staged|bulk|mixed|hybrid]
                     [--log2n 30] [--workload c2|c5] [--sweep FILE] [--ab FILE]
 
 A "step" is one fill of 2^30 uniform doubles from seed
@@ -263,7 +263,8 @@ def run_reference(args) -> None:
 
 # ------------------------------------------------------------------ ours
 ENGINE_NAMES = {"auto": "Auto", "barrett": "Barrett", "montgomery": "Montgomery", "fp64": "FP64",
-                "staged": "Staged", "bulk": "Bulk", "mixed": "Mixed"}
+                "staged": "Staged", "bulk": "Bulk", "mixed": "Mixed",
+                "hybrid": "Hybrid"}
 
 
 def kernel_name(fmt: int, engine: int, paced: bool) -> str:

@@ -65,7 +65,8 @@ typedef enum bcn_engine {
     BCN_ENGINE_FP64 = 3,       /* exact FP64-pipe jump multiply            */
     BCN_ENGINE_STAGED = 4,     /* paper T=1 modified Barrett + TMA bulk store */
     BCN_ENGINE_BULK = 5,       /* FP64 jump streams staged in smem + TMA bulk store */
-    BCN_ENGINE_MIXED = 6       /* DFMA quotient + exact integer remainder   */
+    BCN_ENGINE_MIXED = 6,      /* DFMA quotient + exact integer remainder   */
+    BCN_ENGINE_HYBRID = 7      /* FP64 and Barrett streams side by side (FP64 + IMAD pipes) */
 } bcn_engine;
 
 /* ---- library ---------------------------------------------------------- */

@@ -96,7 +96,7 @@ struct DevCtx {
     int* flag = nullptr;
     void* qscratch = nullptr;         // quality-suite counts / partial sums (grows)
     size_t qscratch_bytes = 0;
-    std::map<int, int> occ;           // (fmt*8+engine) -> blocks per SM
+    std::map<int, int> occ;           // (interleaved*1024 + fmt*64 + engine) -> blocks per SM
     std::mutex occ_mu;                // guards occ
     std::mutex mu;                    // serialises host-buffer fills on this device
     std::mutex small_mu;              // serialises users of digest / flag / qscratch
@@ -198,14 +198,28 @@ bcn_status caller_stream(DevCtx* c, void* stream, cudaStream_t* s) {
     return BCN_OK;
 }
 
+// Hybrid engine split: FP64 streams per lane vector (the rest run Barrett);
+// BCN_HYBRID_KF overrides it for exploration (1 <= KF < streams per lane).
+int hybrid_kf(int fmt) {
+    static const long env = [] {
+        const char* v = std::getenv("BCN_HYBRID_KF");
+        return v ? std::strtol(v, nullptr, 10) : 0L;
+    }();
+    const int vec = fmt == kFmtF32 ? 8 : 4;
+    if (env >= 1 && env < vec) return static_cast<int>(env);
+    return vec - 1;
+}
+
 int resolve_engine(int engine, int fmt) {
+    if (engine == kEngHybrid) return kEngHybridBase + hybrid_kf(fmt);
     if (engine != kEngAuto) return engine;
-    (void)fmt;
     return kEngFP64;  // measured best (profiles/)
 }
 
+bool is_hybrid(int engine) { return engine >= kEngHybridBase; }
+
 int blocks_per_sm(DevCtx* c, int fmt, int engine, bool interleaved) {
-    const int key = (interleaved ? 64 : 0) + fmt * 8 + engine;
+    const int key = (interleaved ? 1024 : 0) + fmt * 64 + engine;
     std::lock_guard<std::mutex> lock(c->occ_mu);
     auto it = c->occ.find(key);
     if (it != c->occ.end()) return it->second;
@@ -254,7 +268,7 @@ uint64_t paced_grid(const DevCtx* c, int engine, uint64_t interleaved_width = 0)
 // 1..4 CTAs per SM: Barrett 3.9-5.6 TB/s, Montgomery 3.3-4.5,
 // tune_engines_cps.jsonl; unpaced: 6.1 / 4.8, ab_f64.jsonl).
 bool paced(DevCtx* c, int fmt, int engine) {
-    return (g_pace_formats.load() >> fmt & 1) && (engine == kEngFP64 || engine == kEngMixed) &&
+    return (g_pace_formats.load() >> fmt & 1) && (engine == kEngFP64 || engine == kEngMixed || is_hybrid(engine)) &&
            pace_gbs(c) > 0.0;
 }
 
@@ -429,7 +443,9 @@ cudaError_t enqueue_region(const FillJob& j, char* dptr, uint64_t slot0, uint64_
     const int isz = format_itemsize(j.fmt);
     // The staged paths are contiguous-only; interleaved regions use the
     // matching direct-store engine.
-    const int engine = j.engine == kEngStaged ? kEngBarrett : j.engine == kEngBulk ? kEngFP64 : j.engine;
+    const int engine = j.engine == kEngStaged ? kEngBarrett
+                       : (j.engine == kEngBulk || is_hybrid(j.engine)) ? kEngFP64
+                                                                        : j.engine;
     const uint64_t addr = reinterpret_cast<uint64_t>(dptr);
     const uint64_t row = 32ull * (32 / isz);
     const uint64_t head = std::min<uint64_t>(count, ((32 - addr % 32) % 32) / isz);
@@ -582,7 +598,7 @@ bcn_status validate_enums(int fmt, int layout, int method, int engine) {
     if (fmt < 0 || fmt > 2) return fail(BCN_ERR_INVALID_ARGUMENT, "fill: unknown format");
     if (layout < 0 || layout > 1) return fail(BCN_ERR_INVALID_ARGUMENT, "fill: unknown layout");
     if (method < 0 || method > 3) return fail(BCN_ERR_INVALID_ARGUMENT, "fill: unknown method");
-    if (engine < 0 || engine > 6) return fail(BCN_ERR_INVALID_ARGUMENT, "fill: unknown engine");
+    if (engine < 0 || engine > 7) return fail(BCN_ERR_INVALID_ARGUMENT, "fill: unknown engine");
     return BCN_OK;
 }
 
@@ -970,6 +986,7 @@ const char* bcn_engine_name(int engine) {
         case BCN_ENGINE_STAGED: return "staged";
         case BCN_ENGINE_BULK: return "bulk";
         case BCN_ENGINE_MIXED: return "mixed";
+        case BCN_ENGINE_HYBRID: return "hybrid";
     }
     return "?";
 }
@@ -1144,7 +1161,7 @@ bcn_status bcn_bench_fill(uint64_t n, uint32_t workers, bcn_layout layout, uint6
     // bench.cpp:102-142 / :241-248, measured on the device.
     if (!exec_seconds || !total_seconds) return fail(BCN_ERR_INVALID_ARGUMENT, "bench_fill: null output");
     if (n == 0 || repeats < 1) return fail(BCN_ERR_INVALID_ARGUMENT, "bench_fill: n and repeats must be >= 1");
-    if (engine < -1 || engine > 6) return fail(BCN_ERR_INVALID_ARGUMENT, "bench_fill: unknown engine");
+    if (engine < -1 || engine > 7) return fail(BCN_ERR_INVALID_ARGUMENT, "bench_fill: unknown engine");
     DeviceGuard guard;
     DevCtx* c = nullptr;
     bcn_status st = get_ctx(device < 0 ? 0 : device, &c);

@@ -33,6 +33,7 @@
 #include <algorithm>
 #include <atomic>
 #include <mutex>
+#include <type_traits>
 
 #include "bcn_kernels.cuh"
 
@@ -133,6 +134,54 @@ struct Eng<kEngMixed> {
     }
 };
 
+// Index-aware view of an engine: a lane's V streams may run on different
+// engines (Hybrid below), so every operation takes the stream's index v
+// inside the lane's vector. The loops over v are fully unrolled, so v is a
+// constant and the per-stream choice folds away at compile time.
+template <class E>
+struct EI {
+    using State = typename E::State;
+    static __device__ __forceinline__ State from(uint64_t z, int) { return E::from_canonical(z); }
+    static __device__ __forceinline__ State mul(State s, const Mult& k, int) { return E::mul(s, k); }
+    static __device__ __forceinline__ uint64_t raw(State s, int) { return E::raw(s); }
+    static __device__ __forceinline__ double unit(State s, int) { return E::unit(s); }
+};
+
+// Hybrid engine: streams v < KF of each lane on the FP64 engine (FP64 pipe),
+// the rest on the Shoup-Barrett engine (IMAD + ALU pipes), so both pipes share
+// the jump multiplies of one row. The state register
+// holds the FP64 state's bits or the canonical residue.
+template <int KF>
+struct Hyb {};
+template <int KF>
+struct EI<Hyb<KF>> {
+    using State = uint64_t;
+    using F = Eng<kEngFP64>;
+    using B = Eng<kEngBarrett>;
+    static __device__ __forceinline__ double d(State s) { return __longlong_as_double(static_cast<long long>(s)); }
+    static __device__ __forceinline__ State u(double x) { return static_cast<State>(__double_as_longlong(x)); }
+    static __device__ __forceinline__ State from(uint64_t z, int v) {
+        return v < KF ? u(F::from_canonical(z)) : B::from_canonical(z);
+    }
+    static __device__ __forceinline__ State mul(State s, const Mult& k, int v) {
+        return v < KF ? u(F::mul(d(s), k)) : B::mul(s, k);
+    }
+    static __device__ __forceinline__ uint64_t raw(State s, int v) { return v < KF ? F::raw(d(s)) : B::raw(s); }
+    static __device__ __forceinline__ double unit(State s, int v) { return v < KF ? F::unit(d(s)) : B::unit(s); }
+};
+
+// Engine id -> index-aware engine. Hybrid ids are kEngHybridBase + KF.
+template <int ENG, bool HYB = (ENG >= kEngHybridBase)>
+struct EngSel {
+    using type = EI<Eng<ENG>>;
+};
+template <int ENG>
+struct EngSel<ENG, true> {
+    using type = EI<Hyb<ENG - kEngHybridBase>>;
+};
+template <int ENG>
+using EngOf = typename EngSel<ENG>::type;
+
 // --------------------------------------------------------------- formats
 template <int FMT>
 struct Fmt;
@@ -153,13 +202,13 @@ struct Fmt<kFmtF32> {
 };
 
 template <int FMT, class E>
-__device__ __forceinline__ uint64_t emit_bits(typename E::State s) {
+__device__ __forceinline__ uint64_t emit_bits(typename E::State s, int v) {
     if constexpr (FMT == kFmtU64) {
-        return E::raw(s);
+        return E::raw(s, v);
     } else if constexpr (FMT == kFmtF64) {
-        return static_cast<uint64_t>(__double_as_longlong(E::unit(s)));
+        return static_cast<uint64_t>(__double_as_longlong(E::unit(s, v)));
     } else {
-        return static_cast<uint64_t>(__float_as_uint(f32_rz_from_unit(E::unit(s))));
+        return static_cast<uint64_t>(__float_as_uint(f32_rz_from_unit(E::unit(s, v))));
     }
 }
 
@@ -171,7 +220,7 @@ __device__ __forceinline__ uint64_t emit_bits(typename E::State s) {
 template <int FMT, class E, int N>
 __device__ __forceinline__ void emit_vec(const typename E::State (&st)[N], uint64_t (&bits)[N]) {
 #pragma unroll
-    for (int v = 0; v < N; ++v) bits[v] = emit_bits<FMT, E>(st[v]);
+    for (int v = 0; v < N; ++v) bits[v] = emit_bits<FMT, E>(st[v], v);
 }
 
 // 32-byte store: st.global.v4.b64 / v8.b32 -> SASS STG.E.256 on sm_100a.
@@ -251,7 +300,7 @@ __device__ __forceinline__ void warp_rows(uint64_t rows, uint64_t nw, uint64_t w
 // 32-byte sectors, so every warp store is one fully coalesced 1 KiB write.
 template <int FMT, int ENG>
 __global__ void __launch_bounds__(kContigThreads) k_fill_contig(const ContigArgs a) {
-    using E = Eng<ENG>;
+    using E = EngOf<ENG>;
     constexpr int V = Fmt<FMT>::kVec;
     constexpr uint64_t ROW = 32ull * V;
     const unsigned lane = threadIdx.x & 31;
@@ -278,7 +327,7 @@ __global__ void __launch_bounds__(kContigThreads) k_fill_contig(const ContigArgs
         uint64_t z = dev_state_from_exp(dev_exp_at(a.e0, r * ROW + lane * V));
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-            st[v] = E::from_canonical(z);
+            st[v] = E::from(z, v);
             if (v + 1 < V) z = step_modified_barrett(z);
         }
     }
@@ -292,7 +341,7 @@ __global__ void __launch_bounds__(kContigThreads) k_fill_contig(const ContigArgs
         emit_vec<FMT, E>(st, bits);
         pack_store<FMT>(p, bits);
 #pragma unroll
-        for (int v = 0; v < V; ++v) st[v] = E::mul(st[v], k);
+        for (int v = 0; v < V; ++v) st[v] = E::mul(st[v], k, v);
         p += pstep;
     }
 }
@@ -338,7 +387,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 
 template <int FMT, int ENG, int MODE>
 __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a) {
-    using E = Eng<ENG>;
+    using E = EngOf<ENG>;
     constexpr bool CONST = MODE == kPacedConstant;
     constexpr bool INTER = MODE == kPacedInterleaved;  // per-stream row-crossing multiplier
     constexpr bool INTER_SEED = INTER || MODE == kPacedInterleavedFixed;
@@ -451,13 +500,13 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
                     const uint64_t c = q % a.width;
                     if constexpr (INTER) col[h][v] = static_cast<uint32_t>(c);
                     const uint64_t j = c * a.wpw + a.i_base + q / a.width;
-                    st[h][v] = E::from_canonical(dev_state_from_exp(dev_exp_at(a.e0, j)));
+                    st[h][v] = E::from(dev_state_from_exp(dev_exp_at(a.e0, j)), v);
                 }
             } else {
                 uint64_t z = dev_state_from_exp(dev_exp_at(a.e0, w_slot + h * D));
 #pragma unroll
                 for (int v = 0; v < V; ++v) {
-                    st[h][v] = E::from_canonical(z);
+                    st[h][v] = E::from(z, v);
                     if (v + 1 < V) z = step_modified_barrett(z);
                 }
             }
@@ -506,12 +555,12 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
 #pragma unroll
             for (int h = 0; h < H; ++h)
 #pragma unroll
-                for (int v = 0; v < V; ++v) st[h][v] = E::mul(st[h][v], sel[h][v]);
+                for (int v = 0; v < V; ++v) st[h][v] = E::mul(st[h][v], sel[h][v], v);
         } else if constexpr (!CONST) {
 #pragma unroll
             for (int h = 0; h < H; ++h)
 #pragma unroll
-                for (int v = 0; v < V; ++v) st[h][v] = E::mul(st[h][v], k);
+                for (int v = 0; v < V; ++v) st[h][v] = E::mul(st[h][v], k, v);
         }
         p += H * hstep;
     }
@@ -520,7 +569,7 @@ __global__ void __launch_bounds__(kPacedThreads) k_fill_paced(const PacedArgs a)
 // -------------------------------------------------------- interleaved fill
 template <int FMT, int ENG>
 __global__ void __launch_bounds__(kContigThreads) k_fill_interleaved(const InterleavedArgs a) {
-    using E = Eng<ENG>;
+    using E = EngOf<ENG>;
     constexpr int V = Fmt<FMT>::kVec;
     constexpr uint64_t ROW = 32ull * V;
     const unsigned lane = threadIdx.x & 31;
@@ -540,7 +589,7 @@ __global__ void __launch_bounds__(kContigThreads) k_fill_interleaved(const Inter
         const uint64_t q = a.q0 + r * ROW + lane * V + v;
         col[v] = static_cast<uint32_t>(q % a.width);
         const uint64_t j = col[v] * a.wpw + a.i_base + q / a.width;
-        st[v] = E::from_canonical(dev_state_from_exp(dev_exp_at(a.e0, j)));
+        st[v] = E::from(dev_state_from_exp(dev_exp_at(a.e0, j)), v);
     }
     char* p = static_cast<char*>(a.out) + (r * ROW + lane * V) * sizeof(typename Fmt<FMT>::Item);
     constexpr uint64_t kRowBytes = ROW * sizeof(typename Fmt<FMT>::Item);
@@ -551,7 +600,7 @@ __global__ void __launch_bounds__(kContigThreads) k_fill_interleaved(const Inter
 #pragma unroll
         for (int v = 0; v < V; ++v) {
             const bool same = col[v] < same_below;
-            st[v] = E::mul(st[v], same ? a.jump_same : a.jump_wrap);
+            st[v] = E::mul(st[v], same ? a.jump_same : a.jump_wrap, v);
             col[v] += same ? adv_same : adv_wrap;
         }
         p += kRowBytes;
@@ -666,7 +715,7 @@ __global__ void __launch_bounds__(kStagedThreads) k_fill_staged(const StagedArgs
 // makes both smem stores of the warp conflict-free.
 template <int FMT, int ENG>
 __global__ void __launch_bounds__(kContigThreads) k_fill_bulk(const ContigArgs a) {
-    using E = Eng<ENG>;
+    using E = EngOf<ENG>;
     using Item = typename Fmt<FMT>::Item;
     constexpr int EPC = 16 / sizeof(Item);           // elements per 16-byte chunk
     constexpr uint64_t ROW = 1024 / sizeof(Item);    // elements per 1 KiB row
@@ -692,7 +741,7 @@ __global__ void __launch_bounds__(kContigThreads) k_fill_bulk(const ContigArgs a
             uint64_t z = dev_state_from_exp(dev_exp_at(a.e0, j0));
 #pragma unroll
             for (int j = 0; j < EPC; ++j) {
-                st[h][c][j] = E::from_canonical(z);
+                st[h][c][j] = E::from(z, j);
                 if (j + 1 < EPC) z = step_modified_barrett(z);
             }
         }
@@ -713,7 +762,7 @@ __global__ void __launch_bounds__(kContigThreads) k_fill_bulk(const ContigArgs a
                 for (int c = 0; c < 2; ++c) {
                     uint64_t bits[EPC];
 #pragma unroll
-                    for (int j = 0; j < EPC; ++j) bits[j] = emit_bits<FMT, E>(st[h][c][j]);
+                    for (int j = 0; j < EPC; ++j) bits[j] = emit_bits<FMT, E>(st[h][c][j], j);
                     uint64_t w0, w1;
                     if constexpr (EPC == 2) {
                         w0 = bits[0];
@@ -731,7 +780,7 @@ __global__ void __launch_bounds__(kContigThreads) k_fill_bulk(const ContigArgs a
 #pragma unroll
             for (int c = 0; c < 2; ++c)
 #pragma unroll
-                for (int j = 0; j < EPC; ++j) st[h][c][j] = E::mul(st[h][c][j], k);
+                for (int j = 0; j < EPC; ++j) st[h][c][j] = E::mul(st[h][c][j], k, j);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
@@ -845,12 +894,12 @@ __device__ __forceinline__ void digest_t(const DigestArgs& a, unsigned long long
 template <int ENG>
 __global__ void __launch_bounds__(256) k_engine_check(const uint64_t* z, const Mult* mult, uint64_t* out,
                                                       uint64_t n, uint32_t chain) {
-    using E = Eng<ENG>;
+    using E = EngOf<ENG>;
     for (uint64_t i = blockIdx.x * 256ull + threadIdx.x; i < n; i += gridDim.x * 256ull) {
         const Mult k = mult[i];
-        typename E::State st = E::from_canonical(z[i]);
-        for (uint32_t r = 0; r < chain; ++r) st = E::mul(st, k);
-        out[i] = E::raw(st);
+        typename E::State st = E::from(z[i], 0);
+        for (uint32_t r = 0; r < chain; ++r) st = E::mul(st, k, 0);
+        out[i] = E::raw(st, 0);
     }
 }
 
@@ -1092,6 +1141,29 @@ cudaError_t counted(cudaError_t e) {
     return e;
 }
 
+// Hybrid engine ids kEngHybridBase + KF: KF FP64 streams per lane vector, the
+// rest Barrett (instantiated for 1 <= KF < V).
+template <int FMT, class F>
+bool hybrid_dispatch(int engine, F&& f) {
+    constexpr int V = Fmt<FMT>::kVec;
+    switch (engine - kEngHybridBase) {
+        case 1: f(std::integral_constant<int, 1>{}); return true;
+        case 2: f(std::integral_constant<int, 2>{}); return true;
+        case 3: f(std::integral_constant<int, 3>{}); return true;
+        default: break;
+    }
+    if constexpr (V == 8) {
+        switch (engine - kEngHybridBase) {
+            case 4: f(std::integral_constant<int, 4>{}); return true;
+            case 5: f(std::integral_constant<int, 5>{}); return true;
+            case 6: f(std::integral_constant<int, 6>{}); return true;
+            case 7: f(std::integral_constant<int, 7>{}); return true;
+            default: break;
+        }
+    }
+    return false;
+}
+
 template <int FMT>
 cudaError_t contig_fmt(int engine, const ContigArgs& a, int grid, int block, cudaStream_t s) {
     switch (engine) {
@@ -1108,7 +1180,10 @@ cudaError_t contig_fmt(int engine, const ContigArgs& a, int grid, int block, cud
             k_fill_contig<FMT, kEngMixed><<<grid, block, 0, s>>>(a);
             break;
         default:
-            return cudaErrorInvalidValue;
+            if (!hybrid_dispatch<FMT>(engine, [&](auto kf) {
+                    k_fill_contig<FMT, kEngHybridBase + decltype(kf)::value><<<grid, block, 0, s>>>(a);
+                }))
+                return cudaErrorInvalidValue;
     }
     return counted(cudaGetLastError());
 }
@@ -1161,7 +1236,13 @@ cudaError_t paced_mode(int engine, const PacedArgs& a, int grid, cudaStream_t s)
     switch (engine) {
         case kEngFP64: k_fill_paced<FMT, kEngFP64, MODE><<<grid, kPacedThreads, 0, s>>>(a); break;
         case kEngMixed: k_fill_paced<FMT, kEngMixed, MODE><<<grid, kPacedThreads, 0, s>>>(a); break;
-        default: return cudaErrorInvalidValue;
+        default:
+            if (MODE != kPacedContiguous ||
+                !hybrid_dispatch<FMT>(engine, [&](auto kf) {
+                    k_fill_paced<FMT, kEngHybridBase + decltype(kf)::value, kPacedContiguous>
+                        <<<grid, kPacedThreads, 0, s>>>(a);
+                }))
+                return cudaErrorInvalidValue;
     }
     return counted(cudaGetLastError());
 }
@@ -1427,6 +1508,13 @@ int contig_blocks_per_sm(int fmt, int engine, int block) {
         case kEngMontgomery: return occupancy(k_fill_contig<F, kEngMontgomery>, block); \
         case kEngFP64: return occupancy(k_fill_contig<F, kEngFP64>, block);          \
         case kEngMixed: return occupancy(k_fill_contig<F, kEngMixed>, block);        \
+        default: {                                                                   \
+            int n = 1;                                                               \
+            hybrid_dispatch<F>(engine, [&](auto kf) {                                \
+                n = occupancy(k_fill_contig<F, kEngHybridBase + decltype(kf)::value>, block); \
+            });                                                                      \
+            return n;                                                                \
+        }                                                                            \
     }
     switch (fmt) {
         case kFmtU64: BCN_OCC(kFmtU64) break;

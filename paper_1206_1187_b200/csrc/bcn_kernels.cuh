@@ -18,8 +18,12 @@ enum Engine : int {
     kEngFP64 = 3,
     kEngStaged = 4,  // paper T=1 modified-Barrett runs, smem transpose, TMA bulk store
     kEngBulk = 5,    // FP64 jump streams, smem-staged 16 KiB tiles, TMA bulk store
-    kEngMixed = 6    // DFMA quotient + integer remainder (fewest FP64 ops)
+    kEngMixed = 6,   // DFMA quotient + integer remainder (fewest FP64 ops)
+    kEngHybrid = 7   // FP64 and Barrett streams side by side in every lane
 };
+// Internal ids of the hybrid engine's instantiations: kEngHybridBase + number
+// of FP64 streams per lane vector (bcn_capi.cu: resolve_engine).
+constexpr int kEngHybridBase = 16;
 
 inline int format_itemsize(int fmt) { return fmt == kFmtF32 ? 4 : 8; }
 

@@ -53,6 +53,7 @@ class Engine(enum.IntEnum):
     Staged = 4
     Bulk = 5
     Mixed = 6
+    Hybrid = 7
 
 
 def layout_name(layout: Layout) -> str:

@@ -156,8 +156,8 @@ def test_physical_index_and_plans_match_reference_semantics(bcn, oracle):
 def test_engine_names(bcn):
     from paper_1206_1187_b200 import _lib
 
-    names = [_lib.lib().bcn_engine_name(i).decode() for i in range(7)]
-    assert names == ["auto", "barrett", "montgomery", "fp64", "staged", "bulk", "mixed"]
+    names = [_lib.lib().bcn_engine_name(i).decode() for i in range(8)]
+    assert names == ["auto", "barrett", "montgomery", "fp64", "staged", "bulk", "mixed", "hybrid"]
     assert bcn.par.Engine(_lib.lib().bcn_auto_engine(1)) in (bcn.Engine.Barrett, bcn.Engine.FP64)
     assert _lib.lib().bcn_last_error() is not None
     assert isinstance(_lib.lib().bcn_launch_count(), int)

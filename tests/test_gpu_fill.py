@@ -6,6 +6,8 @@ from __future__ import annotations
 
 import hashlib
 import os
+import subprocess
+import sys
 
 import numpy as np
 import pytest
@@ -16,7 +18,7 @@ import oracle as O
 pytestmark = pytest.mark.gpu
 
 A0 = O.MIN_SEED
-ENGINES = ["Barrett", "Montgomery", "FP64", "Staged", "Bulk", "Mixed"]
+ENGINES = ["Barrett", "Montgomery", "FP64", "Staged", "Bulk", "Mixed", "Hybrid"]
 FORMATS = [(O.FMT_U64, torch.int64, np.uint64), (O.FMT_F64, torch.float64, np.float64),
            (O.FMT_F32, torch.float32, np.float32)]
 
@@ -71,6 +73,29 @@ def test_engines_formats_bit_exact(bcn, cuda, oracle, engine, fmt):
     got = dev_fill(bcn, n, fmt, engine=engine, base=12345)
     want = oracle.fill(n, fmt, base_offset=12345)
     assert np.array_equal(bits(got), bits(want))
+
+
+def test_hybrid_engine_every_split(cuda):
+    """The hybrid engine with every FP64/Barrett split of a lane's streams
+    (BCN_HYBRID_KF is read once per process, so each split runs in a child)."""
+    code = (
+        "import numpy as np, torch, oracle as O, paper_1206_1187_b200 as B\n"
+        "o = O.Oracle()\n"
+        "for fmt, dt in ((2, torch.float32), (1, torch.float64), (0, torch.int64)):\n"
+        "    if fmt != 2 and KF > 3: continue\n"
+        "    for n in (1, 1000, 3 * 2**16 + 5):\n"
+        "        buf = torch.empty(n, dtype=dt, device='cuda:0')\n"
+        "        B.par.fill_format(buf, B.par.make_plan(n, 1), B.kMinSeedIndex, B.Method.BarrettModified, 777,\n"
+        "                          B.Format(fmt), engine=B.Engine.Hybrid, sync=True)\n"
+        "        v = np.uint32 if fmt == 2 else np.uint64\n"
+        "        assert np.array_equal(buf.cpu().numpy().view(v), o.fill(n, fmt, base_offset=777).view(v)), (KF, fmt, n)\n"
+    )
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for kf in (1, 3, 5, 7):
+        env = dict(os.environ, BCN_HYBRID_KF=str(kf))
+        r = subprocess.run([sys.executable, "-c", f"KF = {kf}\n" + code], cwd=root, env=env,
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-3000:]
 
 
 @pytest.mark.parametrize("offset", [1, 2, 3, 5])
@@ -201,7 +226,7 @@ def test_randomized_plans_against_oracle(bcn, cuda, oracle):
     the column-stable and two-multiplier interleaved paths and the slot kernel."""
     rng = np.random.default_rng(0x1206_1187)
     P = 3706040377703682
-    engines = ["Auto", "Barrett", "Montgomery", "FP64", "Staged", "Bulk", "Mixed"]
+    engines = ["Auto", "Barrett", "Montgomery", "FP64", "Staged", "Bulk", "Mixed", "Hybrid"]
     for case in range(int(os.environ.get("BCN_FUZZ_CASES", "400"))):
         n = int(rng.choice([rng.integers(1, 300), rng.integers(300, 5000), rng.integers(5000, 400000)]))
         workers = int(rng.choice([1, 2, 3, 5, 7, 8, 16, 31, 33, 64, 100, 1000, rng.integers(1, 5000)]))
