@@ -18,7 +18,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libbcnrand_b200.so")
-SOURCES = ["bcn_kernels.cu", "bcn_quality.cu", "bcn_capi.cu"]
+SOURCES = ["bcn_kernels.cu", "bcn_deint_tma.cu", "bcn_quality.cu", "bcn_capi.cu"]
 HEADERS = ["bcn_math.cuh", "bcn_kernels.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

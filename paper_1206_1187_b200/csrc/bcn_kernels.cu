@@ -960,13 +960,15 @@ __global__ void __launch_bounds__(kContigThreads) k_constant(const ConstArgs a) 
 // consecutive logical items leave as one run.
 constexpr unsigned kNarrowMaxWidth = 128;
 
-template <typename T, int ROWS = 64, int BYTES = 512>
+template <typename T, int ROWS = 64, int BYTES = 512, int HALO = 0>
 struct WideTile {
     static constexpr int kRows = ROWS;
+    static constexpr int kHalo = HALO;                                  // rows loaded above the tile
+    static constexpr int kTileRows = ROWS + HALO;
     static constexpr int kCols = BYTES / static_cast<int>(sizeof(T));  // workers
     static constexpr int kPitch = kCols + 1;
-    static constexpr int kLoads = kRows * kCols / 256;                // per thread
-    static_assert(kCols <= 256 && 256 % kCols == 0 && kRows % (256 / kCols) == 0, "tile shape");
+    static constexpr int kLoads = kTileRows * kCols / 256;            // per thread
+    static_assert(kCols <= 256 && 256 % kCols == 0 && kTileRows % (256 / kCols) == 0, "tile shape");
 };
 
 // Tile t -> (first worker, first row).
@@ -982,16 +984,19 @@ __device__ __forceinline__ void wide_origin(const TransposeArgs& a, uint64_t t, 
     }
 }
 
+// Rows [i0 - kHalo, i0 + kRows) x workers [w0, w0 + kCols) into registers
+// (zeros outside the region).
 template <typename T, class G>
 __device__ __forceinline__ void wide_load(const TransposeArgs& a, uint64_t t, uint64_t ntw, uint64_t nrb,
                                           T (&v)[G::kLoads]) {
     const T* in = static_cast<const T*>(a.in);
     uint64_t w0, i0;
     wide_origin<G>(a, t, ntw, nrb, w0, i0);
-    const T* src = in + a.p0 + i0 * a.width + w0;
+    const int64_t top = static_cast<int64_t>(i0) - G::kHalo;
+    const T* src = in + static_cast<int64_t>(a.p0) + top * static_cast<int64_t>(a.width) + static_cast<int64_t>(w0);
     constexpr int kRowStep = 256 / G::kCols;  // rows a thread advances per load
     const int r = threadIdx.x / G::kCols, c = threadIdx.x % G::kCols;
-    if (w0 + G::kCols <= a.width && i0 + G::kRows <= a.rows) {
+    if (w0 + G::kCols <= a.width && top >= 0 && i0 + G::kRows <= a.rows) {
         const T* p = src + static_cast<uint64_t>(r) * a.width + c;
         const uint64_t step = kRowStep * a.width;
 #pragma unroll
@@ -999,15 +1004,27 @@ __device__ __forceinline__ void wide_load(const TransposeArgs& a, uint64_t t, ui
     } else {
 #pragma unroll
         for (int j = 0; j < G::kLoads; ++j) {
-            const int rr = r + kRowStep * j;
-            v[j] = (i0 + rr < a.rows && w0 + c < a.width) ? src[static_cast<uint64_t>(rr) * a.width + c] : T(0);
+            const int64_t rr = r + kRowStep * j;
+            v[j] = (top + rr >= 0 && top + rr < static_cast<int64_t>(a.rows) && w0 + c < a.width)
+                       ? src[rr * static_cast<int64_t>(a.width) + c]
+                       : T(0);
         }
     }
 }
 
-template <typename T, int ROWS, int BYTES>
+// HALO = 0: every worker's run leaves in tile-row blocks [i0, i0 + kRows).
+// HALO = L = 32 / itemsize (sector-aligned stores): worker w's block is shifted
+// down by delta_w = (its output offset at i0) mod L items, so each block starts
+// on a 32-byte sector of the output and every sector is written whole by ONE
+// tile. Unaligned runs otherwise split sectors between two tiles written at
+// different times, and HBM turns each partial sector into a read-modify-write:
+// runs misaligned to 32-byte sectors cost 23% (u64) / 35% (u32) of the rate
+// (profiles/r02/deinterleave_alignment.jsonl). The tile loads HALO extra rows
+// above i0 for the shifted blocks; the first block starts at row 0 and the last
+// one runs to the region end.
+template <typename T, int ROWS, int BYTES, int HALO>
 __global__ void __launch_bounds__(256) k_transpose(const TransposeArgs a) {
-    using G = WideTile<T, ROWS, BYTES>;
+    using G = WideTile<T, ROWS, BYTES, HALO>;
     extern __shared__ __align__(16) unsigned char wide_smem[];
     T* tile = reinterpret_cast<T*>(wide_smem);
     T* out = static_cast<T*>(a.out);
@@ -1026,16 +1043,73 @@ __global__ void __launch_bounds__(256) k_transpose(const TransposeArgs a) {
         if (t + gridDim.x < ntiles) wide_load<T, G>(a, t + gridDim.x, ntw, nrb, v);  // prefetch
         uint64_t w0, i0;
         wide_origin<G>(a, t, ntw, nrb, w0, i0);
-        T* dst = out + w0 * a.wpw + a.i_base + i0;
         const int i = threadIdx.x % G::kRows;  // item within the worker's run
         const int wq = threadIdx.x / G::kRows;  // first worker of this thread
-        if (w0 + G::kCols <= a.width && i0 + G::kRows <= a.rows) {
+        if constexpr (HALO == 0) {
+            T* dst = out + w0 * a.wpw + a.i_base + i0;
+            if (w0 + G::kCols <= a.width && i0 + G::kRows <= a.rows) {
 #pragma unroll 8
-            for (int wl = wq; wl < G::kCols; wl += 256 / G::kRows)
-                dst[wl * a.wpw + i] = tile[i * G::kPitch + wl];
+                for (int wl = wq; wl < G::kCols; wl += 256 / G::kRows)
+                    dst[wl * a.wpw + i] = tile[i * G::kPitch + wl];
+            } else {
+                for (int wl = wq; wl < G::kCols; wl += 256 / G::kRows)
+                    if (w0 + wl < a.width && i0 + i < a.rows) dst[wl * a.wpw + i] = tile[i * G::kPitch + wl];
+            }
         } else {
-            for (int wl = wq; wl < G::kCols; wl += 256 / G::kRows)
-                if (w0 + wl < a.width && i0 + i < a.rows) dst[wl * a.wpw + i] = tile[i * G::kPitch + wl];
+            // Worker w0 + wl: block [j0, j1) of its run, j0 = i0 - delta on a
+            // sector (0 for the first block), j1 = the next block's j0 (the
+            // region end for the last block, which may hold up to kRows + L - 1
+            // items). In tile rows (row 0 = item i0 - kHalo) the block is
+            // [s0, e); the per-quad arithmetic is 32-bit.
+            const bool last = i0 + G::kRows >= a.rows;
+            const uint32_t nw = static_cast<uint32_t>(a.width - w0 < static_cast<uint64_t>(G::kCols) ? a.width - w0 : G::kCols);
+            const uint64_t base0 = w0 * a.wpw + a.i_base;  // item 0 of worker w0
+            const uint32_t phase0 = static_cast<uint32_t>((a.out_mod + base0 + i0) & (HALO - 1));
+            const uint32_t wpw_mod = static_cast<uint32_t>(a.wpw & (HALO - 1));
+            const uint32_t e_last = static_cast<uint32_t>(a.rows - i0) + HALO;  // used when `last`
+            T* q = out + static_cast<int64_t>(base0 + i0) - HALO;
+            {
+                // 16-byte stores of E = 16 / itemsize items. Quads of E rows
+                // start where the output address is 16-byte aligned (tile row
+                // a0 = HALO - delta mod E); a warp takes 4 workers x 8
+                // consecutive quads — with the odd pitch the gathers are
+                // conflict-free (4-byte: bank 4 * quad + worker; 8-byte: each
+                // half warp 2 workers x 8 quads on the 16 even banks) and each
+                // store instruction writes four whole 128-byte lines. Quads cut
+                // by the block ends fall back to single items.
+                constexpr int E = 16 / static_cast<int>(sizeof(T));
+                constexpr int kQ = G::kTileRows / E;  // quads per worker
+                static_assert(kQ % 8 == 0 && G::kCols % 4 == 0, "warp = 4 workers x 8 quads");
+                constexpr int kWarpSteps = G::kCols * kQ / 32;
+                const unsigned lane = threadIdx.x & 31;
+#pragma unroll 2
+                for (int ws = threadIdx.x >> 5; ws < kWarpSteps; ws += 8) {
+                    const uint32_t wl = 4 * (ws % (G::kCols / 4)) + (lane >> 3);
+                    const uint32_t kq = 8 * (ws / (G::kCols / 4)) + (lane & 7);
+                    if (wl >= nw) continue;
+                    const uint32_t delta = (phase0 + wl * wpw_mod) & (HALO - 1);
+                    const uint32_t s0 = i0 != 0 ? HALO - delta : HALO;
+                    const uint32_t e = last ? e_last : G::kRows + HALO - delta;
+                    const uint32_t r0 = ((HALO - delta) & (E - 1)) + E * kq;
+                    if (r0 >= e || r0 + E <= s0) continue;
+                    T* p = q + static_cast<uint64_t>(wl) * a.wpw + r0;
+                    const T* t0 = tile + r0 * G::kPitch + wl;
+                    if (r0 >= s0 && r0 + E <= e) {
+                        if constexpr (E == 4) {
+                            const uint32_t x0 = t0[0], x1 = t0[G::kPitch], x2 = t0[2 * G::kPitch], x3 = t0[3 * G::kPitch];
+                            asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(x0), "r"(x1), "r"(x2),
+                                         "r"(x3)
+                                         : "memory");
+                        } else {
+                            const uint64_t x0 = t0[0], x1 = t0[G::kPitch];
+                            asm volatile("st.global.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(x0), "l"(x1) : "memory");
+                        }
+                    } else {
+                        for (uint32_t c = 0; c < static_cast<uint32_t>(E); ++c)
+                            if (r0 + c >= s0 && r0 + c < e) p[c] = t0[c * G::kPitch];
+                    }
+                }
+            }
         }
         __syncthreads();
     }
@@ -1378,15 +1452,15 @@ cudaError_t launch_constant(const ConstArgs& a, int grid, int block, cudaStream_
 }
 
 namespace {
-template <typename T, int ROWS, int BYTES>
-cudaError_t transpose_wide(const TransposeArgs& a, int sms, cudaStream_t s) {
-    using G = WideTile<T, ROWS, BYTES>;
-    const size_t smem = static_cast<size_t>(G::kRows) * G::kPitch * sizeof(T);
-    cudaFuncSetAttribute(k_transpose<T, ROWS, BYTES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+template <typename T, int ROWS, int BYTES, int HALO>
+cudaError_t transpose_wide_h(const TransposeArgs& a, int sms, cudaStream_t s) {
+    using G = WideTile<T, ROWS, BYTES, HALO>;
+    const size_t smem = static_cast<size_t>(G::kTileRows) * G::kPitch * sizeof(T);
+    cudaFuncSetAttribute(k_transpose<T, ROWS, BYTES, HALO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
     const uint64_t nrb = (a.rows + G::kRows - 1) / G::kRows;
     const uint64_t tiles = ((a.width + G::kCols - 1) / G::kCols) * nrb;
-    const uint64_t cap = static_cast<uint64_t>(sms) * occupancy(k_transpose<T, ROWS, BYTES>, 256, smem);
+    const uint64_t cap = static_cast<uint64_t>(sms) * occupancy(k_transpose<T, ROWS, BYTES, HALO>, 256, smem);
     const uint64_t grid = std::min(tiles, cap);
     // Tile order: with few row blocks per worker (very wide regions: short
     // per-worker runs), walking row blocks fastest keeps every worker's whole
@@ -1395,8 +1469,42 @@ cudaError_t transpose_wide(const TransposeArgs& a, int sms, cudaStream_t s) {
     // 2^28 items; profiles/r01/deinterleave_tile_order.jsonl).
     TransposeArgs b = a;
     b.order = nrb <= 4 * grid ? 1u : 0u;
-    k_transpose<T, ROWS, BYTES><<<static_cast<unsigned>(grid), 256, smem, s>>>(b);
+    k_transpose<T, ROWS, BYTES, HALO><<<static_cast<unsigned>(grid), 256, smem, s>>>(b);
     return counted(cudaGetLastError());
+}
+
+// Sector-aligned blocks suffice: runs aligned to 32-byte sectors but not to
+// 128-byte lines lose only 5-15%, and line-aligned halo blocks (L = 128 B)
+// measured slower there. The halo tiles keep the register footprint of the
+// plain ones for 4-byte items (120 + 8 rows: 2 CTAs per SM) and add 4 rows
+// for 8-byte items (1 CTA per SM either way).
+template <typename T, int ROWS, int BYTES>
+cudaError_t transpose_wide(const TransposeArgs& a, int sms, cudaStream_t s) {
+    constexpr int L = 32 / static_cast<int>(sizeof(T));
+    constexpr int kRowsH = ROWS == 128 ? 128 - L : ROWS;
+    // Runs that keep whole sectors at tile boundaries stay on the plain
+    // kernel; so do 8-byte runs on a 16-byte (half-sector) boundary, which
+    // measured faster plain (W = 200 / 10^6 at 2^30: 5.7 / 5.4 vs 4.6 / 4.7 TB/s)
+    // while 8-byte-aligned runs gain 2-18% with the halo blocks
+    // (profiles/r02/deinterleave_alignment.jsonl).
+    // Short regions (a few blocks per run: < 256 rows for 4-byte, < 1024 for
+    // 8-byte items) and 8-byte regions narrower than two worker blocks also
+    // measured faster plain (-6 to -18% with halo blocks at W = 86 / 100 and
+    // W = 10^6 with 268 rows).
+    constexpr uint64_t kNeed = sizeof(T) == 8 ? 2 : L;
+    const bool aligned_runs = (a.wpw % kNeed == 0) && ((a.out_mod + a.i_base) % kNeed == 0);
+    const bool halo_pays = sizeof(T) == 4 ? a.rows >= 256 : (a.rows >= 1024 && a.width >= 256);
+    // (the 4-byte quad mapping needs a multiple of 32 tile rows)
+    constexpr bool kHaloShape = (kRowsH + L) % (8 * 16 / sizeof(T)) == 0;
+    if constexpr (kHaloShape) {
+        static const int mode = [] {  // BCN_DEINT_ALIGN: 0 never, 1 misaligned runs (default), 2 always
+            const char* v = std::getenv("BCN_DEINT_ALIGN");
+            return v ? static_cast<int>(std::strtol(v, nullptr, 10)) : 1;
+        }();
+        if (mode == 2 || (!aligned_runs && halo_pays && mode == 1))
+            return transpose_wide_h<T, kRowsH, BYTES, L>(a, sms, s);
+    }
+    return transpose_wide_h<T, ROWS, BYTES, 0>(a, sms, s);
 }
 
 // Shared-memory pitch of a narrow 4-byte tile: the scatter writes slot q of
@@ -1434,8 +1542,20 @@ unsigned narrow_pitch_u32(unsigned W, unsigned R) {
     return best;
 }
 
+// BCN_DEINT_TMA=1 routes aligned wide regions through the TMA tile mover
+// (bcn_deint_tma.cu). Off by default: on the regions it can take (rows and runs
+// whole 16-byte chunks) it measured 5.5-5.7 TB/s against 5.9-6.2 for the
+// register pipeline (profiles/r02/deinterleave_tma_vs_registers.jsonl).
+bool tma_deinterleave_enabled() {
+    static const bool on = [] {
+        const char* v = std::getenv("BCN_DEINT_TMA");
+        return v && v[0] == '1';
+    }();
+    return on;
+}
+
 template <typename T>
-cudaError_t transpose_t(const TransposeArgs& a, cudaStream_t s) {
+cudaError_t transpose_t(const TransposeArgs& a, cudaStream_t s, bool allow_tma) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1457,6 +1577,13 @@ cudaError_t transpose_t(const TransposeArgs& a, cudaStream_t s) {
         b.pitch = sizeof(T) == 4 ? narrow_pitch_u32(static_cast<unsigned>(a.width), static_cast<unsigned>(rows_per_tile)) : 0;
         k_transpose_narrow<T><<<static_cast<unsigned>(std::min(tiles, cap)), 256, smem, s>>>(b);
     } else {
+        // Wide regions move through the TMA tile mover (bcn_deint_tma.cu) when
+        // its tensor maps can describe them.
+        if (allow_tma && tma_deinterleave_enabled()) {
+            bool used = false;
+            const cudaError_t e = launch_transpose_tma(a, sms, s, &used);
+            if (e != cudaSuccess || used) return e;
+        }
         // Tile shape sweep (profiles/r01/deinterleave_tiles.jsonl): 128-row
         // tiles win everywhere; 8-byte items prefer 1 KiB input runs unless
         // the last tile column would be mostly empty (e.g. W = 129).
@@ -1498,7 +1625,12 @@ cudaError_t transpose_t(const TransposeArgs& a, cudaStream_t s) {
 
 cudaError_t launch_transpose(const TransposeArgs& a, cudaStream_t s) {
     if (a.rows == 0 || a.width == 0) return cudaSuccess;
-    return a.itemsize == 8 ? transpose_t<uint64_t>(a, s) : transpose_t<uint32_t>(a, s);
+    return a.itemsize == 8 ? transpose_t<uint64_t>(a, s, true) : transpose_t<uint32_t>(a, s, true);
+}
+
+cudaError_t launch_transpose_registers(const TransposeArgs& a, cudaStream_t s) {
+    if (a.rows == 0 || a.width == 0) return cudaSuccess;
+    return a.itemsize == 8 ? transpose_t<uint64_t>(a, s, false) : transpose_t<uint32_t>(a, s, false);
 }
 
 int contig_blocks_per_sm(int fmt, int engine, int block) {

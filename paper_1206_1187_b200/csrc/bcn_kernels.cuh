@@ -144,6 +144,7 @@ struct TransposeArgs {
     uint32_t order;   // wide tiles: 0 = worker blocks vary fastest, 1 = row blocks
     uint32_t pitch;   // narrow tiles: smem row pitch in items (0 = rows | 1)
     uint64_t in_items;  // items of the input buffer from `in` (bulk-copy bounds)
+    uint64_t out_mod;   // (address of `out` / itemsize) mod (32 / itemsize): sector phase of the output
 };
 
 // Launchers (bcn_kernels.cu). Each returns the launch error, if any.
@@ -162,6 +163,11 @@ cudaError_t launch_engine_check(int engine, const uint64_t* z, const Mult* mult,
                                 uint32_t chain, cudaStream_t s);
 cudaError_t launch_constant(const ConstArgs& a, int grid, int block, cudaStream_t s);
 cudaError_t launch_transpose(const TransposeArgs& a, cudaStream_t s);
+// Register-pipelined transposes only (no TMA tile mover).
+cudaError_t launch_transpose_registers(const TransposeArgs& a, cudaStream_t s);
+// TMA tile mover for a wide region (bcn_deint_tma.cu); *used = false when the
+// region cannot be described by its tensor maps (nothing launched).
+cudaError_t launch_transpose_tma(const TransposeArgs& a, int sms, cudaStream_t s, bool* used);
 
 // Quality smoke suite (bcn_quality.cu).
 constexpr int kChiSmemBins = 16384;

@@ -154,6 +154,39 @@ def test_deinterleave_shapes(bcn, cuda, oracle, itemsize):
         assert np.array_equal(got, want), (n, w)
 
 
+@pytest.mark.parametrize("itemsize", [4, 8])
+def test_deinterleave_wide_alignments(bcn, cuda, oracle, itemsize):
+    """Wide deinterleave regions whose physical rows and worker runs take every
+    residue mod 16 bytes (line-aligned halo stores with per-worker shifts,
+    first / last row blocks, both regions) and input / output views misaligned
+    by whole items — against the oracle through the C ABI, with a guard band
+    checking nothing is written outside the output."""
+    import ctypes
+
+    from paper_1206_1187_b200 import _lib
+
+    rng = np.random.default_rng(1187 + itemsize)
+    dt, ndt, sdt = (np.uint32, np.int32, torch.int32) if itemsize == 4 else (np.uint64, np.int64, torch.int64)
+    cases = []
+    for w in (129, 130, 131, 132, 200, 257, 1001, 4098):
+        for rows in (40, 128, 161, 300):
+            for extra in (0, 1, w // 2 + 1):
+                cases.append((w * (rows - 1) + extra if extra else w * rows, w))
+    cases += [(1 << 22, 100003), (3 * 2**20 + 5, 1000000 // 7)]
+    for i, (n, w) in enumerate(cases):
+        off_in, off_out = int(rng.integers(0, 3)), int(rng.integers(0, 3))
+        phys = rng.integers(0, np.iinfo(dt).max, n, dtype=dt, endpoint=True)
+        src = torch.empty(n + off_in, dtype=sdt, device=cuda)
+        src[off_in:].copy_(torch.from_numpy(phys.view(ndt)))
+        dst = torch.full((n + off_out + 8,), -1, dtype=sdt, device=cuda)
+        _lib.call("bcn_deinterleave", ctypes.c_void_p(src[off_in:].data_ptr()),
+                  ctypes.c_void_p(dst[off_out:].data_ptr()), n, w, itemsize, 0, ctypes.c_void_p(0))
+        got = dst.cpu().numpy().view(dt)
+        assert np.array_equal(got[off_out:off_out + n], oracle.deinterleave(phys, w)), (i, n, w, off_in, off_out)
+        assert (got[:off_out] == np.iinfo(dt).max).all() and (got[off_out + n:] == np.iinfo(dt).max).all(), \
+            ("wrote outside the output", i, n, w)
+
+
 def test_randomized_deinterleave_against_oracle(bcn, cuda, oracle):
     """Seeded fuzz over the device deinterleave: random n, W (1 .. 2*10^6,
     log-uniform, n < W included), item size and misaligned device views —

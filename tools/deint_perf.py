@@ -24,7 +24,7 @@ def main() -> None:
         widths = tuple(int(w) for w in sys.argv[1].split(","))
     dev = torch.device("cuda:0")
     stream = torch.cuda.current_stream(dev)
-    n = 1 << 28
+    n = 1 << int(os.environ.get("BCN_DEINT_LOG2N", "28"))
     for dt, isz in ((torch.float64, 8), (torch.float32, 4)):
         buf = torch.empty(n, dtype=dt, device=dev)
         for w in widths:
@@ -37,7 +37,7 @@ def main() -> None:
                 ev[i + 1].record(stream)
             torch.cuda.synchronize()
             ms = statistics.median(ev[i].elapsed_time(ev[i + 1]) for i in range(10))
-            print(json.dumps({"path": "deinterleave", "itemsize": isz, "workers": w, "items": n,
+            print(json.dumps({"path": "deinterleave", "tma": os.environ.get("BCN_DEINT_TMA", "1"), "itemsize": isz, "workers": w, "items": n,
                               "ms": ms, "gbs_rw": 2 * n * isz / ms / 1e6}), flush=True)
         del buf
 
