@@ -1136,6 +1136,10 @@ struct NarrowTile {
     static __host__ __device__ constexpr unsigned rows(unsigned width) {
         return width > 64 ? kItems / width / 16 * 16 : kItems / width / 64 * 64;
     }
+    // Rows per tile with `halo` extra rows above it (k_transpose_narrow_h).
+    static __host__ __device__ constexpr unsigned rows_halo(unsigned width, unsigned halo) {
+        return (kItems / width - halo) / 16 * 16;
+    }
 };
 
 template <typename T>
@@ -1152,6 +1156,79 @@ __device__ __forceinline__ void narrow_load(const TransposeArgs& a, uint64_t r0,
             const unsigned q = threadIdx.x + 256 * j;
             v[j] = q < items ? src[q] : T(0);
         }
+    }
+}
+
+// Narrow tiles with sector-aligned worker blocks (the narrow counterpart of
+// k_transpose<..., HALO>): tile t holds rows [t*R - H, t*R + R) (H = one
+// 32-byte sector of items, loaded as one contiguous span with the R rows), and
+// worker w's block [t*R - delta_w, t*R + R - delta_w) starts on a sector of
+// its output run, so no sector is split between two tiles (split sectors
+// become HBM read-modify-writes: u64 W = 65 / 85 at 2^30 items lose 26 / 17%).
+// R + H whole rows fit the kItems-slot span; R is a multiple of 16. W >= 8.
+template <typename T>
+__global__ void __launch_bounds__(256) k_transpose_narrow_h(const TransposeArgs a) {
+    using G = NarrowTile<T>;
+    constexpr unsigned H = 32 / sizeof(T);
+    extern __shared__ __align__(16) unsigned char narrow_smem[];
+    T* tile = reinterpret_cast<T*>(narrow_smem);
+    T* out = static_cast<T*>(a.out);
+    const unsigned W = static_cast<unsigned>(a.width);
+    const unsigned R = G::rows_halo(W, H);
+    const unsigned P = a.pitch ? a.pitch : ((R + H) | 1);
+    const uint64_t M = ((1ull << 32) + W - 1) / W;
+    const uint64_t ntiles = (a.rows + R - 1) / R;
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // Loaded span of tile t: rows [start, end), smem row = row - (t*R - H).
+    auto span = [&](uint64_t t, uint64_t& start, unsigned& items, unsigned& off) {
+        const uint64_t top = t * R;  // + H
+        start = top >= H ? top - H : 0;
+        const uint64_t end = top + R < a.rows ? top + R : a.rows;
+        items = static_cast<unsigned>((end - start) * W);
+        off = static_cast<unsigned>(start + H - top);
+    };
+    T v[G::kLoads];
+    uint64_t t = blockIdx.x;
+    uint64_t start;
+    unsigned items, off;
+    if (t < ntiles) {
+        span(t, start, items, off);
+        narrow_load<T>(a, start, items, v);
+    }
+    for (; t < ntiles; t += gridDim.x) {
+        span(t, start, items, off);
+#pragma unroll
+        for (unsigned j = 0; j < G::kLoads; ++j) {
+            const unsigned q = threadIdx.x + 256 * j;
+            if (q < items) {
+                const unsigned row = static_cast<unsigned>((q * M) >> 32);
+                tile[(q - row * W) * P + row + off] = v[j];
+            }
+        }
+        __syncthreads();
+        const uint64_t tn = t + gridDim.x;
+        if (tn < ntiles) {
+            uint64_t s2;
+            unsigned i2, o2;
+            span(tn, s2, i2, o2);
+            narrow_load<T>(a, s2, i2, v);  // prefetch
+        }
+        const uint64_t i0 = t * R;
+        const bool last = i0 + R >= a.rows;
+        const uint32_t e_last = static_cast<uint32_t>(a.rows - i0) + H;
+        const uint64_t base_t = a.i_base + i0;
+        const uint32_t wpw_mod = static_cast<uint32_t>(a.wpw & (H - 1));
+        const uint32_t phase_t = static_cast<uint32_t>((a.out_mod + base_t) & (H - 1));
+        for (unsigned col = warp; col < W; col += 8) {
+            const uint32_t delta = (phase_t + col * wpw_mod) & (H - 1);
+            const uint32_t s0 = i0 != 0 ? H - delta : H;
+            const uint32_t e = last ? e_last : R + H - delta;
+            T* d = out + static_cast<int64_t>(col * a.wpw + base_t) - H;
+            const T* sm = tile + col * P;
+#pragma unroll 4
+            for (uint32_t i = s0 + lane; i < e; i += 32) d[i] = sm[i];
+        }
+        __syncthreads();
     }
 }
 
@@ -1554,6 +1631,15 @@ bool tma_deinterleave_enabled() {
     return on;
 }
 
+// BCN_DEINT_NARROW_HALO=0 disables the sector-aligned narrow tiles (A/B switch).
+bool narrow_halo_enabled() {
+    static const bool on = [] {
+        const char* v = std::getenv("BCN_DEINT_NARROW_HALO");
+        return !(v && v[0] == '0');
+    }();
+    return on;
+}
+
 template <typename T>
 cudaError_t transpose_t(const TransposeArgs& a, cudaStream_t s, bool allow_tma) {
     int dev = 0, sms = 148;
@@ -1565,7 +1651,27 @@ cudaError_t transpose_t(const TransposeArgs& a, cudaStream_t s, bool allow_tma) 
     // (W = 100: 5.4 vs 4.9 TB/s, W = 120: 5.8 vs 4.8, W = 128: 5.85 vs 5.5;
     // crossover at W ~ 86; profiles/r01/deinterleave_narrow_vs_wide.jsonl).
     constexpr uint64_t narrow_max = sizeof(T) == 8 ? 85 : kNarrowMaxWidth;
-    if (a.width <= narrow_max) {
+    // Sector-aligned narrow tiles for 8-byte items with W >= 40 whose worker
+    // runs are not sector-aligned: +4 / +13 / +36 / +20% at W = 48 / 63 / 65 /
+    // 85 (2^30 items), +-1% below W = 40. 4-byte items measured slower with
+    // them (the smaller R leaves partial warps in the per-column store loop:
+    // 2.2x the instructions at W = 100), so they keep the plain tiles
+    // (profiles/r02/deinterleave_narrow_halo_ab.jsonl).
+    constexpr uint64_t kSector = 32 / sizeof(T);
+    const bool narrow_halo = sizeof(T) == 8 && a.width >= 40 && a.width <= narrow_max && narrow_halo_enabled() &&
+                             (a.wpw % kSector != 0 || (a.out_mod + a.i_base) % kSector != 0);
+    if (narrow_halo) {
+        using G = NarrowTile<T>;
+        const size_t smem = (G::kItems + kNarrowMaxWidth) * sizeof(T);
+        cudaFuncSetAttribute(k_transpose_narrow_h<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+        const uint64_t rows_per_tile = G::rows_halo(static_cast<unsigned>(a.width), kSector);
+        const uint64_t tiles = (a.rows + rows_per_tile - 1) / rows_per_tile;
+        const uint64_t cap = static_cast<uint64_t>(sms) * occupancy(k_transpose_narrow_h<T>, 256, smem);
+        TransposeArgs b = a;
+        b.pitch = 0;
+        k_transpose_narrow_h<T><<<static_cast<unsigned>(std::min(tiles, cap)), 256, smem, s>>>(b);
+    } else if (a.width <= narrow_max) {
         using G = NarrowTile<T>;
         const size_t smem = (G::kItems + kNarrowMaxWidth) * sizeof(T);
         cudaFuncSetAttribute(k_transpose_narrow<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
