@@ -1660,17 +1660,17 @@ cudaError_t transpose_t(const TransposeArgs& a, cudaStream_t s, bool allow_tma) 
     constexpr uint64_t kSector = 32 / sizeof(T);
     const bool narrow_halo = sizeof(T) == 8 && a.width >= 40 && a.width <= narrow_max && narrow_halo_enabled() &&
                              (a.wpw % kSector != 0 || (a.out_mod + a.i_base) % kSector != 0);
-    if (narrow_halo) {
-        using G = NarrowTile<T>;
-        const size_t smem = (G::kItems + kNarrowMaxWidth) * sizeof(T);
-        cudaFuncSetAttribute(k_transpose_narrow_h<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
+    if (sizeof(T) == 8 && narrow_halo) {
+        using G = NarrowTile<uint64_t>;
+        const size_t smem8 = (G::kItems + kNarrowMaxWidth) * sizeof(uint64_t);
+        cudaFuncSetAttribute(k_transpose_narrow_h<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem8));
         const uint64_t rows_per_tile = G::rows_halo(static_cast<unsigned>(a.width), kSector);
         const uint64_t tiles = (a.rows + rows_per_tile - 1) / rows_per_tile;
-        const uint64_t cap = static_cast<uint64_t>(sms) * occupancy(k_transpose_narrow_h<T>, 256, smem);
+        const uint64_t cap = static_cast<uint64_t>(sms) * occupancy(k_transpose_narrow_h<uint64_t>, 256, smem8);
         TransposeArgs b = a;
         b.pitch = 0;
-        k_transpose_narrow_h<T><<<static_cast<unsigned>(std::min(tiles, cap)), 256, smem, s>>>(b);
+        k_transpose_narrow_h<uint64_t><<<static_cast<unsigned>(std::min(tiles, cap)), 256, smem8, s>>>(b);
     } else if (a.width <= narrow_max) {
         using G = NarrowTile<T>;
         const size_t smem = (G::kItems + kNarrowMaxWidth) * sizeof(T);

@@ -1,4 +1,4 @@
-F=gpurun_out/s17; mkdir -p $F
+F=gpurun_out/s17b; mkdir -p $F
 BCN_FUZZ_CASES_DEINT=600 timeout 900 python -m pytest tests/test_gpu_fill.py -m gpu -q -p no:cacheprovider -k "deinterleave or interleaved" > $F/pytest_deint.log 2>&1; echo "rc=$?" >> $F/pytest_deint.log
 W=8,9,16,31,33,48,63,64,65,85,100,127,128
 for rep in 1 2; do
