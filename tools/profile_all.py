@@ -90,6 +90,11 @@ def main() -> None:
     m = 1 << 28
     B.par.deinterleave(f64[:m], B.par.make_plan(m, 1000, B.Layout.Interleaved))
     B.par.deinterleave(f64[:m], B.par.make_plan(m, 7, B.Layout.Interleaved))
+    # sector-aligned halo tiles: u32 wide (W = 1000), u64 narrow (W = 65), u64 wide (odd runs)
+    B.par.deinterleave(f32[:m], B.par.make_plan(m, 1000, B.Layout.Interleaved))
+    B.par.deinterleave(f64[:m], B.par.make_plan(m, 65, B.Layout.Interleaved))
+    B.par.deinterleave(f64[:m - 3 * 4096], B.par.make_plan(m - 3 * 4096, 4096, B.Layout.Interleaved))
+    fill(f32, B.Format.F32, B.Engine.Hybrid)
     B.par.fill(f64[:m], B.par.make_plan(m, 1), A0, sync=True)
     B.quality.chi_square_uniformity(f64[:m], 1000)
     B.par.fill_residues(u64[:m], B.par.make_plan(m, 1), A0, sync=True)

@@ -67,7 +67,8 @@ def main() -> None:
     # every transpose variant: 16-row narrow tiles (W = 100), 64-worker u32
     # tiles (W = 129), both wide tile orders (W = 300 / 5000 at 400003 items)
     rng = np.random.default_rng(5)
-    for n2, w in ((400003, 100), (400003, 129), (400003, 300), (400003, 5000), (3_000_017, 300)):
+    # + sector-aligned halo tiles: narrow u64 (W = 65), wide u32 (W = 300), wide u64 (3_000_017 / 300)
+    for n2, w in ((400003, 65), (400003, 100), (400003, 129), (400003, 300), (400003, 5000), (3_000_017, 300)):
         for npt, tdt in ((np.uint64, torch.int64), (np.uint32, torch.int32)):
             phys = rng.integers(0, np.iinfo(npt).max, n2, dtype=npt, endpoint=True)
             src = torch.from_numpy(phys.view(np.int64 if npt == np.uint64 else np.int32)).to(dev)
