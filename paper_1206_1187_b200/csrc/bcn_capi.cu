@@ -1348,7 +1348,7 @@ bcn_status bcn_deinterleave(const void* in, void* out, uint64_t n, uint32_t work
     t.order = 0;  // chosen per region by the launcher
     t.pitch = 0;
     t.in_items = n;
-    t.out_mod = (reinterpret_cast<uintptr_t>(dout) / itemsize) % (32 / itemsize);
+    t.out_mod = (reinterpret_cast<uintptr_t>(dout) / itemsize) % (128 / itemsize);
     // Region 1: rows [0, sc) of all workers; region 2: the remaining
     // wpw - sc elements of workers 0..W-2 (parallel.cpp:24-33). One
     // persistent-grid launch per region.

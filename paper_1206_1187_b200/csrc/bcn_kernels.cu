@@ -1578,8 +1578,16 @@ cudaError_t transpose_wide(const TransposeArgs& a, int sms, cudaStream_t s) {
             const char* v = std::getenv("BCN_DEINT_ALIGN");
             return v ? static_cast<int>(std::strtol(v, nullptr, 10)) : 1;
         }();
-        if (mode == 2 || (!aligned_runs && halo_pays && mode == 1))
+        // BCN_DEINT_HALO_LINE=1 (exploration): 128-byte line-aligned blocks
+        static const bool line = [] {
+            const char* v = std::getenv("BCN_DEINT_HALO_LINE");
+            return v && v[0] == '1';
+        }();
+        constexpr int kLine = 128 / static_cast<int>(sizeof(T));
+        if (mode == 2 || (!aligned_runs && halo_pays && mode == 1)) {
+            if (ROWS == 128 && line) return transpose_wide_h<T, 128 - kLine, BYTES, kLine>(a, sms, s);
             return transpose_wide_h<T, kRowsH, BYTES, L>(a, sms, s);
+        }
     }
     return transpose_wide_h<T, ROWS, BYTES, 0>(a, sms, s);
 }

@@ -144,7 +144,7 @@ struct TransposeArgs {
     uint32_t order;   // wide tiles: 0 = worker blocks vary fastest, 1 = row blocks
     uint32_t pitch;   // narrow tiles: smem row pitch in items (0 = rows | 1)
     uint64_t in_items;  // items of the input buffer from `in` (bulk-copy bounds)
-    uint64_t out_mod;   // (address of `out` / itemsize) mod (32 / itemsize): sector phase of the output
+    uint64_t out_mod;   // (address of `out` / itemsize) mod (128 / itemsize): line phase of the output
 };
 
 // Launchers (bcn_kernels.cu). Each returns the launch error, if any.
