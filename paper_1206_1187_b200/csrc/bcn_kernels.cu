@@ -1551,8 +1551,9 @@ cudaError_t transpose_wide_h(const TransposeArgs& a, int sms, cudaStream_t s) {
 }
 
 // Sector-aligned blocks suffice: runs aligned to 32-byte sectors but not to
-// 128-byte lines lose only 5-15%, and line-aligned halo blocks (L = 128 B)
-// measured slower there. The halo tiles keep the register footprint of the
+// 128-byte lines lose only 5-15%, and line-aligned halo blocks (L = 128 B,
+// 96 + 32 / 112 + 16 rows) measured 3-25% slower than sector-aligned ones
+// (profiles/r02/deinterleave_u32_width_and_line_halo.jsonl). The halo tiles keep the register footprint of the
 // plain ones for 4-byte items (120 + 8 rows: 2 CTAs per SM) and add 4 rows
 // for 8-byte items (1 CTA per SM either way).
 template <typename T, int ROWS, int BYTES>
@@ -1578,16 +1579,8 @@ cudaError_t transpose_wide(const TransposeArgs& a, int sms, cudaStream_t s) {
             const char* v = std::getenv("BCN_DEINT_ALIGN");
             return v ? static_cast<int>(std::strtol(v, nullptr, 10)) : 1;
         }();
-        // BCN_DEINT_HALO_LINE=1 (exploration): 128-byte line-aligned blocks
-        static const bool line = [] {
-            const char* v = std::getenv("BCN_DEINT_HALO_LINE");
-            return v && v[0] == '1';
-        }();
-        constexpr int kLine = 128 / static_cast<int>(sizeof(T));
-        if (mode == 2 || (!aligned_runs && halo_pays && mode == 1)) {
-            if (ROWS == 128 && line) return transpose_wide_h<T, 128 - kLine, BYTES, kLine>(a, sms, s);
+        if (mode == 2 || (!aligned_runs && halo_pays && mode == 1))
             return transpose_wide_h<T, kRowsH, BYTES, L>(a, sms, s);
-        }
     }
     return transpose_wide_h<T, ROWS, BYTES, 0>(a, sms, s);
 }
@@ -1658,7 +1651,16 @@ cudaError_t transpose_t(const TransposeArgs& a, cudaStream_t s, bool allow_tma) 
     // block with 1 KiB output runs beats 80-112-row narrow tiles there
     // (W = 100: 5.4 vs 4.9 TB/s, W = 120: 5.8 vs 4.8, W = 128: 5.85 vs 5.5;
     // crossover at W ~ 86; profiles/r01/deinterleave_narrow_vs_wide.jsonl).
-    constexpr uint64_t narrow_max = sizeof(T) == 8 ? 85 : kNarrowMaxWidth;
+    // 4-byte items: narrow tiles up to W = 116, wide 128-worker tiles above
+    // (2^30 items: W = 120 / 124 / 127 wide by 16 / 20 / 26%, even at 2^28;
+    // W = 65 ... 116 narrow ahead or mixed; profiles/r02/
+    // deinterleave_u32_width_and_line_halo.jsonl, deinterleave_u32_crossover.jsonl).
+    // BCN_DEINT_U32_NARROW_MAX overrides the crossover (exploration).
+    static const uint64_t narrow_max_u32 = [] {
+        const char* v = std::getenv("BCN_DEINT_U32_NARROW_MAX");
+        return v ? static_cast<uint64_t>(std::strtoul(v, nullptr, 10)) : uint64_t{116};
+    }();
+    const uint64_t narrow_max = sizeof(T) == 8 ? 85 : narrow_max_u32;
     // Sector-aligned narrow tiles for 8-byte items with W >= 40 whose worker
     // runs are not sector-aligned: +4 / +13 / +36 / +20% at W = 48 / 63 / 65 /
     // 85 (2^30 items), +-1% below W = 40. 4-byte items measured slower with
