@@ -143,7 +143,7 @@ def test_deinterleave_shapes(bcn, cuda, oracle, itemsize):
     dt = np.uint32 if itemsize == 4 else np.uint64
     for n, w in [(1, 1), (5, 9), (100003, 1), (100003, 5), (100003, 7), (65536, 8), (100003, 31),
                  (100003, 32), (100003, 33), (100003, 63), (100003, 64), (100003, 65),
-                 (100003, 129), (300007, 1000), (99999, 99999), (2**21 + 17, 4099),
+                 (100003, 120), (100003, 129), (300007, 1000), (99999, 99999), (2**21 + 17, 4099),
                  (2**27 + 3, 130)]:  # thousands of row blocks per worker: worker-block tile order
         phys = rng.integers(0, np.iinfo(dt).max, n, dtype=dt, endpoint=True)
         plan = bcn.par.make_plan(n, w, bcn.Layout.Interleaved)
