@@ -1067,7 +1067,7 @@ __global__ void __launch_bounds__(256) k_transpose(const TransposeArgs a) {
             const uint32_t phase0 = static_cast<uint32_t>((a.out_mod + base0 + i0) & (HALO - 1));
             const uint32_t wpw_mod = static_cast<uint32_t>(a.wpw & (HALO - 1));
             const uint32_t e_last = static_cast<uint32_t>(a.rows - i0) + HALO;  // used when `last`
-            T* q = out + static_cast<int64_t>(base0 + i0) - HALO;
+            const uint64_t q0 = base0 + i0 - HALO;  // item of tile row 0 (mod 2^64; only rows >= s0 are touched)
             {
                 // 16-byte stores of E = 16 / itemsize items. Quads of E rows
                 // start where the output address is 16-byte aligned (tile row
@@ -1092,7 +1092,7 @@ __global__ void __launch_bounds__(256) k_transpose(const TransposeArgs a) {
                     const uint32_t e = last ? e_last : G::kRows + HALO - delta;
                     const uint32_t r0 = ((HALO - delta) & (E - 1)) + E * kq;
                     if (r0 >= e || r0 + E <= s0) continue;
-                    T* p = q + static_cast<uint64_t>(wl) * a.wpw + r0;
+                    T* p = out + (q0 + static_cast<uint64_t>(wl) * a.wpw + r0);
                     const T* t0 = tile + r0 * G::kPitch + wl;
                     if (r0 >= s0 && r0 + E <= e) {
                         if constexpr (E == 4) {
@@ -1223,10 +1223,10 @@ __global__ void __launch_bounds__(256) k_transpose_narrow_h(const TransposeArgs 
             const uint32_t delta = (phase_t + col * wpw_mod) & (H - 1);
             const uint32_t s0 = i0 != 0 ? H - delta : H;
             const uint32_t e = last ? e_last : R + H - delta;
-            T* d = out + static_cast<int64_t>(col * a.wpw + base_t) - H;
+            const uint64_t d0 = col * a.wpw + base_t - H;  // item of tile row 0 (rows >= s0 >= 1 are touched)
             const T* sm = tile + col * P;
 #pragma unroll 4
-            for (uint32_t i = s0 + lane; i < e; i += 32) d[i] = sm[i];
+            for (uint32_t i = s0 + lane; i < e; i += 32) out[d0 + i] = sm[i];
         }
         __syncthreads();
     }
