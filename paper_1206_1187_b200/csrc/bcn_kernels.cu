@@ -960,15 +960,16 @@ __global__ void __launch_bounds__(kContigThreads) k_constant(const ConstArgs a) 
 // consecutive logical items leave as one run.
 constexpr unsigned kNarrowMaxWidth = 128;
 
-template <typename T, int ROWS = 64, int BYTES = 512, int HALO = 0>
+template <typename T, int ROWS = 64, int BYTES = 512, int HALO = 0, int NT = 256>
 struct WideTile {
+    static constexpr int kThreads = NT;
     static constexpr int kRows = ROWS;
     static constexpr int kHalo = HALO;                                  // rows loaded above the tile
     static constexpr int kTileRows = ROWS + HALO;
     static constexpr int kCols = BYTES / static_cast<int>(sizeof(T));  // workers
     static constexpr int kPitch = kCols + 1;
-    static constexpr int kLoads = kTileRows * kCols / 256;            // per thread
-    static_assert(kCols <= 256 && 256 % kCols == 0 && kTileRows % (256 / kCols) == 0, "tile shape");
+    static constexpr int kLoads = kTileRows * kCols / NT;             // per thread
+    static_assert(kCols <= NT && NT % kCols == 0 && kTileRows % (NT / kCols) == 0, "tile shape");
 };
 
 // Tile t -> (first worker, first row).
@@ -994,7 +995,7 @@ __device__ __forceinline__ void wide_load(const TransposeArgs& a, uint64_t t, ui
     wide_origin<G>(a, t, ntw, nrb, w0, i0);
     const int64_t top = static_cast<int64_t>(i0) - G::kHalo;
     const T* src = in + static_cast<int64_t>(a.p0) + top * static_cast<int64_t>(a.width) + static_cast<int64_t>(w0);
-    constexpr int kRowStep = 256 / G::kCols;  // rows a thread advances per load
+    constexpr int kRowStep = G::kThreads / G::kCols;  // rows a thread advances per load
     const int r = threadIdx.x / G::kCols, c = threadIdx.x % G::kCols;
     if (w0 + G::kCols <= a.width && top >= 0 && i0 + G::kRows <= a.rows) {
         const T* p = src + static_cast<uint64_t>(r) * a.width + c;
@@ -1022,16 +1023,16 @@ __device__ __forceinline__ void wide_load(const TransposeArgs& a, uint64_t t, ui
 // (profiles/r02/deinterleave_alignment.jsonl). The tile loads HALO extra rows
 // above i0 for the shifted blocks; the first block starts at row 0 and the last
 // one runs to the region end.
-template <typename T, int ROWS, int BYTES, int HALO>
-__global__ void __launch_bounds__(256) k_transpose(const TransposeArgs a) {
-    using G = WideTile<T, ROWS, BYTES, HALO>;
+template <typename T, int ROWS, int BYTES, int HALO, int NT = 256>
+__global__ void __launch_bounds__(NT) k_transpose(const TransposeArgs a) {
+    using G = WideTile<T, ROWS, BYTES, HALO, NT>;
     extern __shared__ __align__(16) unsigned char wide_smem[];
     T* tile = reinterpret_cast<T*>(wide_smem);
     T* out = static_cast<T*>(a.out);
     const uint64_t ntw = (a.width + G::kCols - 1) / G::kCols;
     const uint64_t nrb = (a.rows + G::kRows - 1) / G::kRows;
     const uint64_t ntiles = ntw * nrb;
-    constexpr int kRowStep = 256 / G::kCols;
+    constexpr int kRowStep = NT / G::kCols;
     const int r = threadIdx.x / G::kCols, c = threadIdx.x % G::kCols;
     T v[G::kLoads];
     uint64_t t = blockIdx.x;
@@ -1049,10 +1050,10 @@ __global__ void __launch_bounds__(256) k_transpose(const TransposeArgs a) {
             T* dst = out + w0 * a.wpw + a.i_base + i0;
             if (w0 + G::kCols <= a.width && i0 + G::kRows <= a.rows) {
 #pragma unroll 8
-                for (int wl = wq; wl < G::kCols; wl += 256 / G::kRows)
+                for (int wl = wq; wl < G::kCols; wl += NT / G::kRows)
                     dst[wl * a.wpw + i] = tile[i * G::kPitch + wl];
             } else {
-                for (int wl = wq; wl < G::kCols; wl += 256 / G::kRows)
+                for (int wl = wq; wl < G::kCols; wl += NT / G::kRows)
                     if (w0 + wl < a.width && i0 + i < a.rows) dst[wl * a.wpw + i] = tile[i * G::kPitch + wl];
             }
         } else {
@@ -1083,7 +1084,7 @@ __global__ void __launch_bounds__(256) k_transpose(const TransposeArgs a) {
                 constexpr int kWarpSteps = G::kCols * kQ / 32;
                 const unsigned lane = threadIdx.x & 31;
 #pragma unroll 2
-                for (int ws = threadIdx.x >> 5; ws < kWarpSteps; ws += 8) {
+                for (int ws = threadIdx.x >> 5; ws < kWarpSteps; ws += NT / 32) {
                     const uint32_t wl = 4 * (ws % (G::kCols / 4)) + (lane >> 3);
                     const uint32_t kq = 8 * (ws / (G::kCols / 4)) + (lane & 7);
                     if (wl >= nw) continue;
@@ -1142,18 +1143,19 @@ struct NarrowTile {
     }
 };
 
-template <typename T>
+template <typename T, unsigned NT = 256>
 __device__ __forceinline__ void narrow_load(const TransposeArgs& a, uint64_t r0, unsigned items,
-                                            T (&v)[NarrowTile<T>::kLoads]) {
+                                            T (&v)[NarrowTile<T>::kItems / NT]) {
     using G = NarrowTile<T>;
+    constexpr unsigned kLoads = G::kItems / NT;
     const T* src = static_cast<const T*>(a.in) + a.p0 + r0 * a.width;
     if (items == G::kItems) {
 #pragma unroll
-        for (unsigned j = 0; j < G::kLoads; ++j) v[j] = src[threadIdx.x + 256 * j];
+        for (unsigned j = 0; j < kLoads; ++j) v[j] = src[threadIdx.x + NT * j];
     } else {
 #pragma unroll
-        for (unsigned j = 0; j < G::kLoads; ++j) {
-            const unsigned q = threadIdx.x + 256 * j;
+        for (unsigned j = 0; j < kLoads; ++j) {
+            const unsigned q = threadIdx.x + NT * j;
             v[j] = q < items ? src[q] : T(0);
         }
     }
@@ -1166,8 +1168,8 @@ __device__ __forceinline__ void narrow_load(const TransposeArgs& a, uint64_t r0,
 // its output run, so no sector is split between two tiles (split sectors
 // become HBM read-modify-writes: u64 W = 65 / 85 at 2^30 items lose 26 / 17%).
 // R + H whole rows fit the kItems-slot span; R is a multiple of 16. W >= 8.
-template <typename T>
-__global__ void __launch_bounds__(256) k_transpose_narrow_h(const TransposeArgs a) {
+template <typename T, unsigned NT = 256>
+__global__ void __launch_bounds__(NT) k_transpose_narrow_h(const TransposeArgs a) {
     using G = NarrowTile<T>;
     constexpr unsigned H = 32 / sizeof(T);
     extern __shared__ __align__(16) unsigned char narrow_smem[];
@@ -1187,19 +1189,20 @@ __global__ void __launch_bounds__(256) k_transpose_narrow_h(const TransposeArgs 
         items = static_cast<unsigned>((end - start) * W);
         off = static_cast<unsigned>(start + H - top);
     };
-    T v[G::kLoads];
+    constexpr unsigned kLoads = G::kItems / NT;
+    T v[kLoads];
     uint64_t t = blockIdx.x;
     uint64_t start;
     unsigned items, off;
     if (t < ntiles) {
         span(t, start, items, off);
-        narrow_load<T>(a, start, items, v);
+        narrow_load<T, NT>(a, start, items, v);
     }
     for (; t < ntiles; t += gridDim.x) {
         span(t, start, items, off);
 #pragma unroll
-        for (unsigned j = 0; j < G::kLoads; ++j) {
-            const unsigned q = threadIdx.x + 256 * j;
+        for (unsigned j = 0; j < kLoads; ++j) {
+            const unsigned q = threadIdx.x + NT * j;
             if (q < items) {
                 const unsigned row = static_cast<unsigned>((q * M) >> 32);
                 tile[(q - row * W) * P + row + off] = v[j];
@@ -1211,7 +1214,7 @@ __global__ void __launch_bounds__(256) k_transpose_narrow_h(const TransposeArgs 
             uint64_t s2;
             unsigned i2, o2;
             span(tn, s2, i2, o2);
-            narrow_load<T>(a, s2, i2, v);  // prefetch
+            narrow_load<T, NT>(a, s2, i2, v);  // prefetch
         }
         const uint64_t i0 = t * R;
         const bool last = i0 + R >= a.rows;
@@ -1219,7 +1222,7 @@ __global__ void __launch_bounds__(256) k_transpose_narrow_h(const TransposeArgs 
         const uint64_t base_t = a.i_base + i0;
         const uint32_t wpw_mod = static_cast<uint32_t>(a.wpw & (H - 1));
         const uint32_t phase_t = static_cast<uint32_t>((a.out_mod + base_t) & (H - 1));
-        for (unsigned col = warp; col < W; col += 8) {
+        for (unsigned col = warp; col < W; col += NT / 32) {
             const uint32_t delta = (phase_t + col * wpw_mod) & (H - 1);
             const uint32_t s0 = i0 != 0 ? H - delta : H;
             const uint32_t e = last ? e_last : R + H - delta;
@@ -1232,8 +1235,8 @@ __global__ void __launch_bounds__(256) k_transpose_narrow_h(const TransposeArgs 
     }
 }
 
-template <typename T>
-__global__ void __launch_bounds__(256) k_transpose_narrow(const TransposeArgs a) {
+template <typename T, unsigned NT = 256>
+__global__ void __launch_bounds__(NT) k_transpose_narrow(const TransposeArgs a) {
     using G = NarrowTile<T>;
     extern __shared__ __align__(16) unsigned char narrow_smem[];
     T* tile = reinterpret_cast<T*>(narrow_smem);
@@ -1248,14 +1251,15 @@ __global__ void __launch_bounds__(256) k_transpose_narrow(const TransposeArgs a)
     auto rows_of = [&](uint64_t t) {
         return static_cast<unsigned>(a.rows - t * R < R ? a.rows - t * R : R);
     };
-    T v[G::kLoads];
+    constexpr unsigned kLoads = G::kItems / NT;
+    T v[kLoads];
     uint64_t t = blockIdx.x;
-    if (t < ntiles) narrow_load<T>(a, t * R, rows_of(t) * W, v);
+    if (t < ntiles) narrow_load<T, NT>(a, t * R, rows_of(t) * W, v);
     for (; t < ntiles; t += gridDim.x) {
         const unsigned nr = rows_of(t), items = nr * W;
 #pragma unroll
-        for (unsigned j = 0; j < G::kLoads; ++j) {
-            const unsigned q = threadIdx.x + 256 * j;
+        for (unsigned j = 0; j < kLoads; ++j) {
+            const unsigned q = threadIdx.x + NT * j;
             if (q < items) {
                 const unsigned row = static_cast<unsigned>((q * M) >> 32);
                 tile[(q - row * W) * P + row] = v[j];
@@ -1263,13 +1267,13 @@ __global__ void __launch_bounds__(256) k_transpose_narrow(const TransposeArgs a)
         }
         __syncthreads();
         const uint64_t tn = t + gridDim.x;
-        if (tn < ntiles) narrow_load<T>(a, tn * R, rows_of(tn) * W, v);  // prefetch
+        if (tn < ntiles) narrow_load<T, NT>(a, tn * R, rows_of(tn) * W, v);  // prefetch
         T* dst = out + a.i_base + t * R;
         if (W < 8) {
             for (unsigned col = 0; col < W; ++col)
-                for (unsigned i = threadIdx.x; i < nr; i += 256) dst[col * a.wpw + i] = tile[col * P + i];
+                for (unsigned i = threadIdx.x; i < nr; i += NT) dst[col * a.wpw + i] = tile[col * P + i];
         } else {
-            for (unsigned col = warp; col < W; col += 8) {
+            for (unsigned col = warp; col < W; col += NT / 32) {
                 T* d = dst + col * a.wpw;
                 const T* s = tile + col * P;
 #pragma unroll 4
@@ -1529,15 +1533,15 @@ cudaError_t launch_constant(const ConstArgs& a, int grid, int block, cudaStream_
 }
 
 namespace {
-template <typename T, int ROWS, int BYTES, int HALO>
-cudaError_t transpose_wide_h(const TransposeArgs& a, int sms, cudaStream_t s) {
-    using G = WideTile<T, ROWS, BYTES, HALO>;
+template <typename T, int ROWS, int BYTES, int HALO, int NT = 256>
+cudaError_t transpose_wide_nt(const TransposeArgs& a, int sms, cudaStream_t s) {
+    using G = WideTile<T, ROWS, BYTES, HALO, NT>;
     const size_t smem = static_cast<size_t>(G::kTileRows) * G::kPitch * sizeof(T);
-    cudaFuncSetAttribute(k_transpose<T, ROWS, BYTES, HALO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_transpose<T, ROWS, BYTES, HALO, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
     const uint64_t nrb = (a.rows + G::kRows - 1) / G::kRows;
     const uint64_t tiles = ((a.width + G::kCols - 1) / G::kCols) * nrb;
-    const uint64_t cap = static_cast<uint64_t>(sms) * occupancy(k_transpose<T, ROWS, BYTES, HALO>, 256, smem);
+    const uint64_t cap = static_cast<uint64_t>(sms) * occupancy(k_transpose<T, ROWS, BYTES, HALO, NT>, NT, smem);
     const uint64_t grid = std::min(tiles, cap);
     // Tile order: with few row blocks per worker (very wide regions: short
     // per-worker runs), walking row blocks fastest keeps every worker's whole
@@ -1546,8 +1550,29 @@ cudaError_t transpose_wide_h(const TransposeArgs& a, int sms, cudaStream_t s) {
     // 2^28 items; profiles/r01/deinterleave_tile_order.jsonl).
     TransposeArgs b = a;
     b.order = nrb <= 4 * grid ? 1u : 0u;
-    k_transpose<T, ROWS, BYTES, HALO><<<static_cast<unsigned>(grid), 256, smem, s>>>(b);
+    k_transpose<T, ROWS, BYTES, HALO, NT><<<static_cast<unsigned>(grid), NT, smem, s>>>(b);
     return counted(cudaGetLastError());
+}
+
+// Threads per wide CTA: 512 for 8-byte regions narrower than one 128-worker
+// block (W = 86 / 100: +11 / +5%: one partly empty column block needs more
+// warps in flight), 256 otherwise (512 measured -2 to -10% at W >= 120 and
+// mixed for u32; profiles/r02/deinterleave_wide_threads.jsonl).
+// BCN_DEINT_WIDE_THREADS = 256 | 512 forces one (A/B switch).
+template <typename T>
+int wide_threads(uint64_t width) {
+    static const int env = [] {
+        const char* v = std::getenv("BCN_DEINT_WIDE_THREADS");
+        return v ? static_cast<int>(std::strtol(v, nullptr, 10)) : 0;
+    }();
+    if (env) return env;
+    return sizeof(T) == 8 && width < 128 ? 512 : 256;
+}
+
+template <typename T, int ROWS, int BYTES, int HALO>
+cudaError_t transpose_wide_h(const TransposeArgs& a, int sms, cudaStream_t s) {
+    if (wide_threads<T>(a.width) == 512) return transpose_wide_nt<T, ROWS, BYTES, HALO, 512>(a, sms, s);
+    return transpose_wide_nt<T, ROWS, BYTES, HALO, 256>(a, sms, s);
 }
 
 // Sector-aligned blocks suffice: runs aligned to 32-byte sectors but not to
@@ -1641,6 +1666,19 @@ bool narrow_halo_enabled() {
     return on;
 }
 
+// Threads per narrow CTA: 512 for 8-byte items (twice the warps on the same
+// 64 KiB tile: +7-10% at W = 2 / 16 / 31 / 33 / 64, equal elsewhere), 256 for
+// 4-byte items (512 measured 0-6% slower; profiles/r02/deinterleave_narrow_threads.jsonl).
+// BCN_DEINT_NARROW_THREADS=256|512 overrides (A/B switch).
+template <typename T>
+int narrow_threads() {
+    static const int nt = [] {
+        const char* v = std::getenv("BCN_DEINT_NARROW_THREADS");
+        return v ? static_cast<int>(std::strtol(v, nullptr, 10)) : (sizeof(T) == 8 ? 512 : 256);
+    }();
+    return nt;
+}
+
 template <typename T>
 cudaError_t transpose_t(const TransposeArgs& a, cudaStream_t s, bool allow_tma) {
     int dev = 0, sms = 148;
@@ -1673,25 +1711,39 @@ cudaError_t transpose_t(const TransposeArgs& a, cudaStream_t s, bool allow_tma) 
     if (sizeof(T) == 8 && narrow_halo) {
         using G = NarrowTile<uint64_t>;
         const size_t smem8 = (G::kItems + kNarrowMaxWidth) * sizeof(uint64_t);
-        cudaFuncSetAttribute(k_transpose_narrow_h<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem8));
         const uint64_t rows_per_tile = G::rows_halo(static_cast<unsigned>(a.width), kSector);
         const uint64_t tiles = (a.rows + rows_per_tile - 1) / rows_per_tile;
-        const uint64_t cap = static_cast<uint64_t>(sms) * occupancy(k_transpose_narrow_h<uint64_t>, 256, smem8);
         TransposeArgs b = a;
         b.pitch = 0;
-        k_transpose_narrow_h<uint64_t><<<static_cast<unsigned>(std::min(tiles, cap)), 256, smem8, s>>>(b);
+        if (narrow_threads<uint64_t>() == 512) {
+            cudaFuncSetAttribute(k_transpose_narrow_h<uint64_t, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem8));
+            const uint64_t cap = static_cast<uint64_t>(sms) * occupancy(k_transpose_narrow_h<uint64_t, 512>, 512, smem8);
+            k_transpose_narrow_h<uint64_t, 512><<<static_cast<unsigned>(std::min(tiles, cap)), 512, smem8, s>>>(b);
+        } else {
+            cudaFuncSetAttribute(k_transpose_narrow_h<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem8));
+            const uint64_t cap = static_cast<uint64_t>(sms) * occupancy(k_transpose_narrow_h<uint64_t>, 256, smem8);
+            k_transpose_narrow_h<uint64_t><<<static_cast<unsigned>(std::min(tiles, cap)), 256, smem8, s>>>(b);
+        }
     } else if (a.width <= narrow_max) {
         using G = NarrowTile<T>;
         const size_t smem = (G::kItems + kNarrowMaxWidth) * sizeof(T);
-        cudaFuncSetAttribute(k_transpose_narrow<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
         const uint64_t rows_per_tile = G::rows(static_cast<unsigned>(a.width));
         const uint64_t tiles = (a.rows + rows_per_tile - 1) / rows_per_tile;
-        const uint64_t cap = static_cast<uint64_t>(sms) * occupancy(k_transpose_narrow<T>, 256, smem);
         TransposeArgs b = a;
         b.pitch = sizeof(T) == 4 ? narrow_pitch_u32(static_cast<unsigned>(a.width), static_cast<unsigned>(rows_per_tile)) : 0;
-        k_transpose_narrow<T><<<static_cast<unsigned>(std::min(tiles, cap)), 256, smem, s>>>(b);
+        if (narrow_threads<T>() == 512) {
+            cudaFuncSetAttribute(k_transpose_narrow<T, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem));
+            const uint64_t cap = static_cast<uint64_t>(sms) * occupancy(k_transpose_narrow<T, 512>, 512, smem);
+            k_transpose_narrow<T, 512><<<static_cast<unsigned>(std::min(tiles, cap)), 512, smem, s>>>(b);
+        } else {
+            cudaFuncSetAttribute(k_transpose_narrow<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem));
+            const uint64_t cap = static_cast<uint64_t>(sms) * occupancy(k_transpose_narrow<T>, 256, smem);
+            k_transpose_narrow<T><<<static_cast<unsigned>(std::min(tiles, cap)), 256, smem, s>>>(b);
+        }
     } else {
         // Wide regions move through the TMA tile mover (bcn_deint_tma.cu) when
         // its tensor maps can describe them.

@@ -1,0 +1,7 @@
+F=gpurun_out/s22; mkdir -p $F
+BCN_DEINT_NARROW_THREADS=512 timeout 900 python -m pytest tests/test_gpu_fill.py -m gpu -q -p no:cacheprovider -k "deinterleave" > $F/pytest.log 2>&1; echo "rc=$?" >> $F/pytest.log
+W=2,7,16,31,33,64,65,85,100,116
+for rep in 1 2; do for nt in 256 512; do
+BCN_DEINT_NARROW_THREADS=$nt BCN_DEINT_LOG2N=30 timeout 300 python tools/deint_perf.py $W | sed "s/^{/{\"nt\": $nt, \"log2n\": 30, /" >> $F/d.jsonl 2>>$F/err.txt
+BCN_DEINT_NARROW_THREADS=$nt BCN_DEINT_LOG2N=28 timeout 300 python tools/deint_perf.py $W | sed "s/^{/{\"nt\": $nt, \"log2n\": 28, /" >> $F/d.jsonl 2>>$F/err.txt
+done; done
