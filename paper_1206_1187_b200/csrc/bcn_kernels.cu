@@ -1023,8 +1023,8 @@ __device__ __forceinline__ void wide_load(const TransposeArgs& a, uint64_t t, ui
 // (profiles/r02/deinterleave_alignment.jsonl). The tile loads HALO extra rows
 // above i0 for the shifted blocks; the first block starts at row 0 and the last
 // one runs to the region end.
-template <typename T, int ROWS, int BYTES, int HALO, int NT = 256>
-__global__ void __launch_bounds__(NT) k_transpose(const TransposeArgs a) {
+template <typename T, int ROWS, int BYTES, int HALO, int NT>
+__device__ __forceinline__ void transpose_wide_body(const TransposeArgs& a) {
     using G = WideTile<T, ROWS, BYTES, HALO, NT>;
     extern __shared__ __align__(16) unsigned char wide_smem[];
     T* tile = reinterpret_cast<T*>(wide_smem);
@@ -1114,6 +1114,14 @@ __global__ void __launch_bounds__(NT) k_transpose(const TransposeArgs a) {
         }
         __syncthreads();
     }
+}
+
+// The wide kernel. __launch_bounds__ without a minimum-blocks argument: with
+// one, ptxas spends more registers (the 4-byte narrow tile went from 124 to 168,
+// one CTA per SM instead of two, -10%).
+template <typename T, int ROWS, int BYTES, int HALO, int NT = 256>
+__global__ void __launch_bounds__(NT) k_transpose(const TransposeArgs a) {
+    transpose_wide_body<T, ROWS, BYTES, HALO, NT>(a);
 }
 
 // Narrow regions (width <= kNarrowMaxWidth workers for 4-byte items, <= 85
@@ -1235,8 +1243,8 @@ __global__ void __launch_bounds__(NT) k_transpose_narrow_h(const TransposeArgs a
     }
 }
 
-template <typename T, unsigned NT = 256>
-__global__ void __launch_bounds__(NT) k_transpose_narrow(const TransposeArgs a) {
+template <typename T, unsigned NT>
+__device__ __forceinline__ void transpose_narrow_body(const TransposeArgs& a) {
     using G = NarrowTile<T>;
     extern __shared__ __align__(16) unsigned char narrow_smem[];
     T* tile = reinterpret_cast<T*>(narrow_smem);
@@ -1282,6 +1290,11 @@ __global__ void __launch_bounds__(NT) k_transpose_narrow(const TransposeArgs a) 
         }
         __syncthreads();
     }
+}
+
+template <typename T, unsigned NT = 256>
+__global__ void __launch_bounds__(NT) k_transpose_narrow(const TransposeArgs a) {
+    transpose_narrow_body<T, NT>(a);
 }
 
 // ============================================================ launchers
@@ -1535,13 +1548,13 @@ cudaError_t launch_constant(const ConstArgs& a, int grid, int block, cudaStream_
 namespace {
 template <typename T, int ROWS, int BYTES, int HALO, int NT = 256>
 cudaError_t transpose_wide_nt(const TransposeArgs& a, int sms, cudaStream_t s) {
+    constexpr auto kernel = k_transpose<T, ROWS, BYTES, HALO, NT>;
     using G = WideTile<T, ROWS, BYTES, HALO, NT>;
     const size_t smem = static_cast<size_t>(G::kTileRows) * G::kPitch * sizeof(T);
-    cudaFuncSetAttribute(k_transpose<T, ROWS, BYTES, HALO, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     const uint64_t nrb = (a.rows + G::kRows - 1) / G::kRows;
     const uint64_t tiles = ((a.width + G::kCols - 1) / G::kCols) * nrb;
-    const uint64_t cap = static_cast<uint64_t>(sms) * occupancy(k_transpose<T, ROWS, BYTES, HALO, NT>, NT, smem);
+    const uint64_t cap = static_cast<uint64_t>(sms) * occupancy(kernel, NT, smem);
     const uint64_t grid = std::min(tiles, cap);
     // Tile order: with few row blocks per worker (very wide regions: short
     // per-worker runs), walking row blocks fastest keeps every worker's whole
@@ -1550,7 +1563,7 @@ cudaError_t transpose_wide_nt(const TransposeArgs& a, int sms, cudaStream_t s) {
     // 2^28 items; profiles/r01/deinterleave_tile_order.jsonl).
     TransposeArgs b = a;
     b.order = nrb <= 4 * grid ? 1u : 0u;
-    k_transpose<T, ROWS, BYTES, HALO, NT><<<static_cast<unsigned>(grid), NT, smem, s>>>(b);
+    kernel<<<static_cast<unsigned>(grid), NT, smem, s>>>(b);
     return counted(cudaGetLastError());
 }
 
