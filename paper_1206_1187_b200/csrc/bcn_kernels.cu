@@ -1567,10 +1567,10 @@ cudaError_t transpose_wide_nt(const TransposeArgs& a, int sms, cudaStream_t s) {
     return counted(cudaGetLastError());
 }
 
-// Threads per wide CTA: 512 for 8-byte regions narrower than one 128-worker
-// block (W = 86 / 100: +11 / +5%: one partly empty column block needs more
-// warps in flight), 256 otherwise (512 measured -2 to -10% at W >= 120 and
-// mixed for u32; profiles/r02/deinterleave_wide_threads.jsonl).
+// Threads per wide CTA: 512 for 8-byte regions of at most 104 workers (one
+// mostly empty 128-worker column block; W = 86 / 100: +11 / +5%), 256
+// otherwise (512 measured -6 to -9% at W = 120 / 127 and mixed for u32;
+// profiles/r02/deinterleave_wide_threads.jsonl).
 // BCN_DEINT_WIDE_THREADS = 256 | 512 forces one (A/B switch).
 template <typename T>
 int wide_threads(uint64_t width) {
@@ -1579,7 +1579,7 @@ int wide_threads(uint64_t width) {
         return v ? static_cast<int>(std::strtol(v, nullptr, 10)) : 0;
     }();
     if (env) return env;
-    return sizeof(T) == 8 && width < 128 ? 512 : 256;
+    return sizeof(T) == 8 && width <= 104 ? 512 : 256;
 }
 
 template <typename T, int ROWS, int BYTES, int HALO>
