@@ -960,14 +960,17 @@ __global__ void __launch_bounds__(kContigThreads) k_constant(const ConstArgs a) 
 // consecutive logical items leave as one run.
 constexpr unsigned kNarrowMaxWidth = 128;
 
-template <typename T, int ROWS = 64, int BYTES = 512, int HALO = 0, int NT = 256>
+template <typename T, int ROWS = 64, int BYTES = 512, int HALO = 0, int NT = 256, int PADJ = 0>
 struct WideTile {
     static constexpr int kThreads = NT;
     static constexpr int kRows = ROWS;
     static constexpr int kHalo = HALO;                                  // rows loaded above the tile
     static constexpr int kTileRows = ROWS + HALO;
     static constexpr int kCols = BYTES / static_cast<int>(sizeof(T));  // workers
-    static constexpr int kPitch = kCols + 1;
+    // Odd pitch: conflict-free column reads of single items. Halo tiles of
+    // 4-byte items whose run length is 1 mod 4 add PADJ = 2 (see the quad
+    // gathers in transpose_wide_body).
+    static constexpr int kPitch = kCols + 1 + PADJ;
     static constexpr int kLoads = kTileRows * kCols / NT;             // per thread
     static_assert(kCols <= NT && NT % kCols == 0 && kTileRows % (NT / kCols) == 0, "tile shape");
 };
@@ -1023,9 +1026,9 @@ __device__ __forceinline__ void wide_load(const TransposeArgs& a, uint64_t t, ui
 // (profiles/r02/deinterleave_alignment.jsonl). The tile loads HALO extra rows
 // above i0 for the shifted blocks; the first block starts at row 0 and the last
 // one runs to the region end.
-template <typename T, int ROWS, int BYTES, int HALO, int NT>
+template <typename T, int ROWS, int BYTES, int HALO, int NT, int PADJ>
 __device__ __forceinline__ void transpose_wide_body(const TransposeArgs& a) {
-    using G = WideTile<T, ROWS, BYTES, HALO, NT>;
+    using G = WideTile<T, ROWS, BYTES, HALO, NT, PADJ>;
     extern __shared__ __align__(16) unsigned char wide_smem[];
     T* tile = reinterpret_cast<T*>(wide_smem);
     T* out = static_cast<T*>(a.out);
@@ -1034,12 +1037,13 @@ __device__ __forceinline__ void transpose_wide_body(const TransposeArgs& a) {
     const uint64_t ntiles = ntw * nrb;
     constexpr int kRowStep = NT / G::kCols;
     const int r = threadIdx.x / G::kCols, c = threadIdx.x % G::kCols;
+    constexpr int P = G::kPitch;
     T v[G::kLoads];
     uint64_t t = blockIdx.x;
     if (t < ntiles) wide_load<T, G>(a, t, ntw, nrb, v);
     for (; t < ntiles; t += gridDim.x) {
 #pragma unroll
-        for (int j = 0; j < G::kLoads; ++j) tile[(r + kRowStep * j) * G::kPitch + c] = v[j];
+        for (int j = 0; j < G::kLoads; ++j) tile[(r + kRowStep * j) * P + c] = v[j];
         __syncthreads();
         if (t + gridDim.x < ntiles) wide_load<T, G>(a, t + gridDim.x, ntw, nrb, v);  // prefetch
         uint64_t w0, i0;
@@ -1072,12 +1076,14 @@ __device__ __forceinline__ void transpose_wide_body(const TransposeArgs& a) {
             {
                 // 16-byte stores of E = 16 / itemsize items. Quads of E rows
                 // start where the output address is 16-byte aligned (tile row
-                // a0 = HALO - delta mod E); a warp takes 4 workers x 8
-                // consecutive quads — with the odd pitch the gathers are
-                // conflict-free (4-byte: bank 4 * quad + worker; 8-byte: each
-                // half warp 2 workers x 8 quads on the 16 even banks) and each
-                // store instruction writes four whole 128-byte lines. Quads cut
-                // by the block ends fall back to single items.
+                // a0 = HALO - delta mod E, which differs between workers); a
+                // warp takes 4 workers x 8 consecutive quads, so each store
+                // instruction writes four whole 128-byte lines. The gathers
+                // are conflict-free for even wpw and 2-way for odd wpw with
+                // the pitch the launcher picks (PADJ; exhaustive check over
+                // run phases; 8 workers x 4 quads is conflict-free at pitch 130
+                // but its 64-byte store segments measured 13-18% slower).
+                // Quads cut by the block ends fall back to single items.
                 constexpr int E = 16 / static_cast<int>(sizeof(T));
                 constexpr int kQ = G::kTileRows / E;  // quads per worker
                 static_assert(kQ % 8 == 0 && G::kCols % 4 == 0, "warp = 4 workers x 8 quads");
@@ -1094,20 +1100,20 @@ __device__ __forceinline__ void transpose_wide_body(const TransposeArgs& a) {
                     const uint32_t r0 = ((HALO - delta) & (E - 1)) + E * kq;
                     if (r0 >= e || r0 + E <= s0) continue;
                     T* p = out + (q0 + static_cast<uint64_t>(wl) * a.wpw + r0);
-                    const T* t0 = tile + r0 * G::kPitch + wl;
+                    const T* t0 = tile + r0 * P + wl;
                     if (r0 >= s0 && r0 + E <= e) {
                         if constexpr (E == 4) {
-                            const uint32_t x0 = t0[0], x1 = t0[G::kPitch], x2 = t0[2 * G::kPitch], x3 = t0[3 * G::kPitch];
+                            const uint32_t x0 = t0[0], x1 = t0[P], x2 = t0[2 * P], x3 = t0[3 * P];
                             asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(x0), "r"(x1), "r"(x2),
                                          "r"(x3)
                                          : "memory");
                         } else {
-                            const uint64_t x0 = t0[0], x1 = t0[G::kPitch];
+                            const uint64_t x0 = t0[0], x1 = t0[P];
                             asm volatile("st.global.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(x0), "l"(x1) : "memory");
                         }
                     } else {
                         for (uint32_t c = 0; c < static_cast<uint32_t>(E); ++c)
-                            if (r0 + c >= s0 && r0 + c < e) p[c] = t0[c * G::kPitch];
+                            if (r0 + c >= s0 && r0 + c < e) p[c] = t0[c * P];
                     }
                 }
             }
@@ -1119,9 +1125,9 @@ __device__ __forceinline__ void transpose_wide_body(const TransposeArgs& a) {
 // The wide kernel. __launch_bounds__ without a minimum-blocks argument: with
 // one, ptxas spends more registers (the 4-byte narrow tile went from 124 to 168,
 // one CTA per SM instead of two, -10%).
-template <typename T, int ROWS, int BYTES, int HALO, int NT = 256>
+template <typename T, int ROWS, int BYTES, int HALO, int NT = 256, int PADJ = 0>
 __global__ void __launch_bounds__(NT) k_transpose(const TransposeArgs a) {
-    transpose_wide_body<T, ROWS, BYTES, HALO, NT>(a);
+    transpose_wide_body<T, ROWS, BYTES, HALO, NT, PADJ>(a);
 }
 
 // Narrow regions (width <= kNarrowMaxWidth workers for 4-byte items, <= 85
@@ -1546,10 +1552,10 @@ cudaError_t launch_constant(const ConstArgs& a, int grid, int block, cudaStream_
 }
 
 namespace {
-template <typename T, int ROWS, int BYTES, int HALO, int NT = 256>
+template <typename T, int ROWS, int BYTES, int HALO, int NT = 256, int PADJ = 0>
 cudaError_t transpose_wide_nt(const TransposeArgs& a, int sms, cudaStream_t s) {
-    constexpr auto kernel = k_transpose<T, ROWS, BYTES, HALO, NT>;
-    using G = WideTile<T, ROWS, BYTES, HALO, NT>;
+    constexpr auto kernel = k_transpose<T, ROWS, BYTES, HALO, NT, PADJ>;
+    using G = WideTile<T, ROWS, BYTES, HALO, NT, PADJ>;
     const size_t smem = static_cast<size_t>(G::kTileRows) * G::kPitch * sizeof(T);
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     const uint64_t nrb = (a.rows + G::kRows - 1) / G::kRows;
@@ -1585,6 +1591,10 @@ int wide_threads(uint64_t width) {
 template <typename T, int ROWS, int BYTES, int HALO>
 cudaError_t transpose_wide_h(const TransposeArgs& a, int sms, cudaStream_t s) {
     if (wide_threads<T>(a.width) == 512) return transpose_wide_nt<T, ROWS, BYTES, HALO, 512>(a, sms, s);
+    // 4-byte halo tiles with a run length of 1 mod 4: pitch + 2 halves the
+    // quad-gather bank conflicts (4-way -> 2-way; 3 mod 4 is 2-way already).
+    if constexpr (HALO != 0 && sizeof(T) == 4)
+        if (a.wpw % 4 == 1) return transpose_wide_nt<T, ROWS, BYTES, HALO, 256, 2>(a, sms, s);
     return transpose_wide_nt<T, ROWS, BYTES, HALO, 256>(a, sms, s);
 }
 

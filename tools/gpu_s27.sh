@@ -1,0 +1,7 @@
+F=gpurun_out/s29; mkdir -p $F
+BCN_FUZZ_CASES_DEINT=400 timeout 900 python -m pytest tests/test_gpu_fill.py -m gpu -q -p no:cacheprovider -k "deinterleave" > $F/pytest.log 2>&1; echo "rc=$?" >> $F/pytest.log
+W=129,200,1000,5003,100003,1000000
+for l in 30 28; do BCN_DEINT_LOG2N=$l timeout 300 python tools/deint_perf.py $W | sed "s/^{/{\"log2n\": $l, /" >> $F/d.jsonl 2>>$F/err.txt; done
+timeout 600 python tools/deint_align.py > $F/align.jsonl 2>> $F/err.txt
+timeout 600 ncu --set full --clock-control none -k regex:k_transpose -c 1 -o /tmp/u32_129 python tools/deint_one.py --w 129 --isz 4 --log2n 30 > $F/ncu.log 2>&1
+ncu -i /tmp/u32_129.ncu-rep --page raw --csv > $F/raw_129.csv 2>/dev/null
