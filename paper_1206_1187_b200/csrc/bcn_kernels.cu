@@ -1240,10 +1240,14 @@ __global__ void __launch_bounds__(NT) k_transpose_narrow_h(const TransposeArgs a
             const uint32_t delta = (phase_t + col * wpw_mod) & (H - 1);
             const uint32_t s0 = i0 != 0 ? H - delta : H;
             const uint32_t e = last ? e_last : R + H - delta;
-            const uint64_t d0 = col * a.wpw + base_t - H;  // item of tile row 0 (rows >= s0 >= 1 are touched)
-            const T* sm = tile + col * P;
-#pragma unroll 4
-            for (uint32_t i = s0 + lane; i < e; i += 32) out[d0 + i] = sm[i];
+            // rows [s0, e) of the column; a plain loop (an unrolled one with
+            // per-column trip counts cost ~50 instructions of remainder logic
+            // per column: 2.2x the plain kernel's instruction count)
+            T* d = out + (col * a.wpw + base_t - H + s0);
+            const T* sm = tile + col * P + s0;
+            const uint32_t len = e - s0;
+#pragma unroll 1
+            for (uint32_t i = lane; i < len; i += 32) d[i] = sm[i];
         }
         __syncthreads();
     }
@@ -1724,30 +1728,31 @@ cudaError_t transpose_t(const TransposeArgs& a, cudaStream_t s, bool allow_tma) 
     const uint64_t narrow_max = sizeof(T) == 8 ? 85 : narrow_max_u32;
     // Sector-aligned narrow tiles for 8-byte items with W >= 40 whose worker
     // runs are not sector-aligned: +4 / +13 / +36 / +20% at W = 48 / 63 / 65 /
-    // 85 (2^30 items), +-1% below W = 40. 4-byte items measured slower with
-    // them (the smaller R leaves partial warps in the per-column store loop:
-    // 2.2x the instructions at W = 100), so they keep the plain tiles
-    // (profiles/r02/deinterleave_narrow_halo_ab.jsonl).
+    // 85 (2^30 items), +-1% below W = 40. 4-byte items measured 7-38% slower
+    // with them even with a lean store loop: the 8 halo rows and the
+    // rounding of R to 16 cut the rows per 8192-slot tile (W = 116: 48 + 8
+    // rows against 64), so they keep the plain tiles
+    // (profiles/r02/deinterleave_narrow_halo_ab.jsonl, deinterleave_narrow_halo_u32_lean.jsonl).
     constexpr uint64_t kSector = 32 / sizeof(T);
     const bool narrow_halo = sizeof(T) == 8 && a.width >= 40 && a.width <= narrow_max && narrow_halo_enabled() &&
                              (a.wpw % kSector != 0 || (a.out_mod + a.i_base) % kSector != 0);
-    if (sizeof(T) == 8 && narrow_halo) {
-        using G = NarrowTile<uint64_t>;
-        const size_t smem8 = (G::kItems + kNarrowMaxWidth) * sizeof(uint64_t);
+    if (narrow_halo) {
+        using G = NarrowTile<T>;
+        const size_t smemh = (G::kItems + kNarrowMaxWidth) * sizeof(T);
         const uint64_t rows_per_tile = G::rows_halo(static_cast<unsigned>(a.width), kSector);
         const uint64_t tiles = (a.rows + rows_per_tile - 1) / rows_per_tile;
         TransposeArgs b = a;
         b.pitch = 0;
-        if (narrow_threads<uint64_t>() == 512) {
-            cudaFuncSetAttribute(k_transpose_narrow_h<uint64_t, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem8));
-            const uint64_t cap = static_cast<uint64_t>(sms) * occupancy(k_transpose_narrow_h<uint64_t, 512>, 512, smem8);
-            k_transpose_narrow_h<uint64_t, 512><<<static_cast<unsigned>(std::min(tiles, cap)), 512, smem8, s>>>(b);
+        if (narrow_threads<T>() == 512) {
+            cudaFuncSetAttribute(k_transpose_narrow_h<T, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smemh));
+            const uint64_t cap = static_cast<uint64_t>(sms) * occupancy(k_transpose_narrow_h<T, 512>, 512, smemh);
+            k_transpose_narrow_h<T, 512><<<static_cast<unsigned>(std::min(tiles, cap)), 512, smemh, s>>>(b);
         } else {
-            cudaFuncSetAttribute(k_transpose_narrow_h<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem8));
-            const uint64_t cap = static_cast<uint64_t>(sms) * occupancy(k_transpose_narrow_h<uint64_t>, 256, smem8);
-            k_transpose_narrow_h<uint64_t><<<static_cast<unsigned>(std::min(tiles, cap)), 256, smem8, s>>>(b);
+            cudaFuncSetAttribute(k_transpose_narrow_h<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smemh));
+            const uint64_t cap = static_cast<uint64_t>(sms) * occupancy(k_transpose_narrow_h<T>, 256, smemh);
+            k_transpose_narrow_h<T><<<static_cast<unsigned>(std::min(tiles, cap)), 256, smemh, s>>>(b);
         }
     } else if (a.width <= narrow_max) {
         using G = NarrowTile<T>;
