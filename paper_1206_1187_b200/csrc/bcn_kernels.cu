@@ -1138,9 +1138,9 @@ __global__ void __launch_bounds__(NT) k_transpose(const TransposeArgs a) {
 // width by a multiply-high), and each worker's R consecutive logical items
 // leave as one run (all warps on one worker for width < 8, one worker per
 // warp otherwise).
-template <typename T>
+template <typename T, unsigned KITEMS = 8192>
 struct NarrowTile {
-    static constexpr unsigned kItems = 8192;  // slots per tile (64 / 32 KiB)
+    static constexpr unsigned kItems = KITEMS;  // slots per tile (default 64 / 32 KiB)
     static constexpr unsigned kLoads = kItems / 256;
     // Rows per tile: as many whole rows as fit, a multiple of 64 (512-byte
     // output runs for u64) — except for W in (64, 128], where that leaves 64
@@ -1157,10 +1157,10 @@ struct NarrowTile {
     }
 };
 
-template <typename T, unsigned NT = 256>
+template <typename T, unsigned NT = 256, unsigned KITEMS = 8192>
 __device__ __forceinline__ void narrow_load(const TransposeArgs& a, uint64_t r0, unsigned items,
-                                            T (&v)[NarrowTile<T>::kItems / NT]) {
-    using G = NarrowTile<T>;
+                                            T (&v)[KITEMS / NT]) {
+    using G = NarrowTile<T, KITEMS>;
     constexpr unsigned kLoads = G::kItems / NT;
     const T* src = static_cast<const T*>(a.in) + a.p0 + r0 * a.width;
     if (items == G::kItems) {
@@ -1253,9 +1253,9 @@ __global__ void __launch_bounds__(NT) k_transpose_narrow_h(const TransposeArgs a
     }
 }
 
-template <typename T, unsigned NT>
+template <typename T, unsigned NT, unsigned KITEMS>
 __device__ __forceinline__ void transpose_narrow_body(const TransposeArgs& a) {
-    using G = NarrowTile<T>;
+    using G = NarrowTile<T, KITEMS>;
     extern __shared__ __align__(16) unsigned char narrow_smem[];
     T* tile = reinterpret_cast<T*>(narrow_smem);
     T* out = static_cast<T*>(a.out);
@@ -1272,7 +1272,7 @@ __device__ __forceinline__ void transpose_narrow_body(const TransposeArgs& a) {
     constexpr unsigned kLoads = G::kItems / NT;
     T v[kLoads];
     uint64_t t = blockIdx.x;
-    if (t < ntiles) narrow_load<T, NT>(a, t * R, rows_of(t) * W, v);
+    if (t < ntiles) narrow_load<T, NT, KITEMS>(a, t * R, rows_of(t) * W, v);
     for (; t < ntiles; t += gridDim.x) {
         const unsigned nr = rows_of(t), items = nr * W;
 #pragma unroll
@@ -1285,7 +1285,7 @@ __device__ __forceinline__ void transpose_narrow_body(const TransposeArgs& a) {
         }
         __syncthreads();
         const uint64_t tn = t + gridDim.x;
-        if (tn < ntiles) narrow_load<T, NT>(a, tn * R, rows_of(tn) * W, v);  // prefetch
+        if (tn < ntiles) narrow_load<T, NT, KITEMS>(a, tn * R, rows_of(tn) * W, v);  // prefetch
         T* dst = out + a.i_base + t * R;
         if (W < 8) {
             for (unsigned col = 0; col < W; ++col)
@@ -1302,9 +1302,9 @@ __device__ __forceinline__ void transpose_narrow_body(const TransposeArgs& a) {
     }
 }
 
-template <typename T, unsigned NT = 256>
+template <typename T, unsigned NT = 256, unsigned KITEMS = 8192>
 __global__ void __launch_bounds__(NT) k_transpose_narrow(const TransposeArgs a) {
-    transpose_narrow_body<T, NT>(a);
+    transpose_narrow_body<T, NT, KITEMS>(a);
 }
 
 // ============================================================ launchers
@@ -1611,7 +1611,7 @@ cudaError_t transpose_wide_h(const TransposeArgs& a, int sms, cudaStream_t s) {
 template <typename T, int ROWS, int BYTES>
 cudaError_t transpose_wide(const TransposeArgs& a, int sms, cudaStream_t s) {
     constexpr int L = 32 / static_cast<int>(sizeof(T));
-    constexpr int kRowsH = ROWS == 128 ? 128 - L : ROWS;
+    constexpr int kRowsH = ROWS >= 128 ? ROWS - L : ROWS;
     // Runs that keep whole sectors at tile boundaries stay on the plain
     // kernel; so do 8-byte runs on a 16-byte (half-sector) boundary, which
     // measured faster plain (W = 200 / 10^6 at 2^30: 5.7 / 5.4 vs 4.6 / 4.7 TB/s)
@@ -1684,6 +1684,21 @@ bool tma_deinterleave_enabled() {
     return on;
 }
 
+// Narrow widths above this take 16384-slot tiles on 512 threads (twice the
+// rows per tile, halving the sectors split between tiles): 4-byte items from
+// W = 16, +2-26% (2^30 items: W = 63 / 85 / 100 / 116: +16 / +16 / +26 /
+// +14%); W = 9 -2 to -5%; 8-byte items 0 to -6%, so they keep 8192 slots
+// (profiles/r02/deinterleave_narrow_big_tiles.jsonl). Knobs
+// BCN_DEINT_NARROW_BIG_MIN_U32 / _U64 override (A/B switch).
+template <typename T>
+unsigned narrow_big_min() {
+    static const unsigned v = [] {
+        const char* e = std::getenv(sizeof(T) == 4 ? "BCN_DEINT_NARROW_BIG_MIN_U32" : "BCN_DEINT_NARROW_BIG_MIN_U64");
+        return e ? static_cast<unsigned>(std::strtoul(e, nullptr, 10)) : (sizeof(T) == 4 ? 15u : 0x7fffffffu);
+    }();
+    return v;
+}
+
 // BCN_DEINT_NARROW_HALO=0 disables the sector-aligned narrow tiles (A/B switch).
 bool narrow_halo_enabled() {
     static const bool on = [] {
@@ -1716,14 +1731,14 @@ cudaError_t transpose_t(const TransposeArgs& a, cudaStream_t s, bool allow_tma) 
     // block with 1 KiB output runs beats 80-112-row narrow tiles there
     // (W = 100: 5.4 vs 4.9 TB/s, W = 120: 5.8 vs 4.8, W = 128: 5.85 vs 5.5;
     // crossover at W ~ 86; profiles/r01/deinterleave_narrow_vs_wide.jsonl).
-    // 4-byte items: narrow tiles up to W = 116, wide 128-worker tiles above
-    // (2^30 items: W = 120 / 124 / 127 wide by 16 / 20 / 26%, even at 2^28;
-    // W = 65 ... 116 narrow ahead or mixed; profiles/r02/
-    // deinterleave_u32_width_and_line_halo.jsonl, deinterleave_u32_crossover.jsonl).
+    // 4-byte items: narrow tiles up to W = 128 with the 16384-slot tiles
+    // (with 8192-slot tiles the crossover was W = 116: W = 120 / 124 / 127
+    // went wide, +16-26%; profiles/r02/deinterleave_u32_crossover.jsonl,
+    // deinterleave_narrow_big_tiles.jsonl).
     // BCN_DEINT_U32_NARROW_MAX overrides the crossover (exploration).
     static const uint64_t narrow_max_u32 = [] {
         const char* v = std::getenv("BCN_DEINT_U32_NARROW_MAX");
-        return v ? static_cast<uint64_t>(std::strtoul(v, nullptr, 10)) : uint64_t{116};
+        return v ? static_cast<uint64_t>(std::strtoul(v, nullptr, 10)) : uint64_t{128};
     }();
     const uint64_t narrow_max = sizeof(T) == 8 ? 85 : narrow_max_u32;
     // Sector-aligned narrow tiles for 8-byte items with W >= 40 whose worker
@@ -1754,6 +1769,18 @@ cudaError_t transpose_t(const TransposeArgs& a, cudaStream_t s, bool allow_tma) 
             const uint64_t cap = static_cast<uint64_t>(sms) * occupancy(k_transpose_narrow_h<T>, 256, smemh);
             k_transpose_narrow_h<T><<<static_cast<unsigned>(std::min(tiles, cap)), 256, smemh, s>>>(b);
         }
+    } else if (a.width > narrow_big_min<T>() && a.width <= narrow_max) {
+        // 16384-slot tiles on 512 threads (twice the rows per tile)
+        using G = NarrowTile<T, 16384>;
+        const size_t smem = (G::kItems + kNarrowMaxWidth) * sizeof(T);
+        const uint64_t rows_per_tile = G::rows(static_cast<unsigned>(a.width));
+        const uint64_t tiles = (a.rows + rows_per_tile - 1) / rows_per_tile;
+        TransposeArgs b = a;
+        b.pitch = sizeof(T) == 4 ? narrow_pitch_u32(static_cast<unsigned>(a.width), static_cast<unsigned>(rows_per_tile)) : 0;
+        cudaFuncSetAttribute(k_transpose_narrow<T, 512, 16384>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+        const uint64_t cap = static_cast<uint64_t>(sms) * occupancy(k_transpose_narrow<T, 512, 16384>, 512, smem);
+        k_transpose_narrow<T, 512, 16384><<<static_cast<unsigned>(std::min(tiles, cap)), 512, smem, s>>>(b);
     } else if (a.width <= narrow_max) {
         using G = NarrowTile<T>;
         const size_t smem = (G::kItems + kNarrowMaxWidth) * sizeof(T);
