@@ -1,6 +1,6 @@
 # Final evidence pass on the round-2 code (one gpurun call); outputs under gpurun_out/final.
 set -x
-F=gpurun_out/final2
+F=gpurun_out/final3
 mkdir -p $F
 nvidia-smi --query-gpu=name,serial,clocks.sm,clocks.max.sm,power.draw,power.limit --format=csv > $F/smi.txt
 python -c "import __graft_entry__ as g; g.smoke()" > $F/smoke.log 2>&1; echo "smoke rc=$?" >> $F/smoke.log
