@@ -187,6 +187,28 @@ def test_deinterleave_wide_alignments(bcn, cuda, oracle, itemsize):
             ("wrote outside the output", i, n, w)
 
 
+def test_deinterleave_tma_tile_mover_opt_in(cuda):
+    """The opt-in TMA tile mover (BCN_DEINT_TMA=1, bcn_deint_tma.cu) on wide
+    regions whose rows and runs are whole 16-byte chunks (the only ones its
+    tensor maps take), with tails below one store box and the < ko last
+    workers; other shapes fall back inside the same call. Env is read once
+    per process, so the check runs in a child."""
+    code = (
+        "import numpy as np, torch, oracle as O, paper_1206_1187_b200 as B\n"
+        "o = O.Oracle(); rng = np.random.default_rng(3)\n"
+        "for isz, dt, sdt in ((4, np.uint32, np.int32), (8, np.uint64, np.int64)):\n"
+        "    for n, w in ((1024 * 4096, 1024), (1024 * 4096 + 17, 1024), (4096 * 300, 4096), (200 * 777, 200), (1001 * 500, 1001)):\n"
+        "        phys = rng.integers(0, np.iinfo(dt).max, n, dtype=dt, endpoint=True)\n"
+        "        src = torch.from_numpy(phys.view(sdt)).to('cuda:0')\n"
+        "        got = B.par.deinterleave(src, B.par.make_plan(n, w, B.Layout.Interleaved)).cpu().numpy().view(dt)\n"
+        "        assert np.array_equal(got, o.deinterleave(phys, w)), (isz, n, w)\n"
+    )
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, BCN_DEINT_TMA="1")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-3000:]
+
+
 def test_randomized_deinterleave_against_oracle(bcn, cuda, oracle):
     """Seeded fuzz over the device deinterleave: random n, W (1 .. 2*10^6,
     log-uniform, n < W included), item size and misaligned device views —
